@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""bench.py -- BASELINE metric "AES-128 ECB encrypt/decrypt Gbps at 1/2/4/8 B200;
+% of HBM roofline" on BASELINE config 2 ("AES-128 ECB encrypt and decrypt,
+1 GiB random buffer, 1 B200"), one 1 GiB shard per GPU (weak scaling).
+
+A STEP = one pass of the whole hot path over one
+batch: aes_expand_key (host) -> aes_ecb_encrypt(1 GiB) -> aes_ecb_decrypt of
+that ciphertext (1 GiB).  Payload per step and rank = 2 GiB.
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+For N > 1 launch under torchrun (one rank per GPU; NCCL only for barrier and
+the MAX/SUM of scalars -- no data-path collective).
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GIB = 1 << 30
+METRIC = "AES-128 ECB encrypt/decrypt Gbps at 1/2/4/8 B200; % of HBM roofline"
+WORKLOAD = "AES-128 ECB encrypt and decrypt, 1 GiB random buffer, 1 B200"
+KEYBITS = 128
+NR = 10
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--bytes-per-gpu", type=int, default=GIB)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor()
+
+
+# ---------------------------------------------------------------------------
+# oracle timing (cpu_baseline / --impl reference): the oracle as it stands
+# ---------------------------------------------------------------------------
+def time_oracle(target_s: float, cores: int):
+    """Encrypt + decrypt a bounded sample of the same workload (the first
+    blocks of the same synthetic stream) with the oracle on `cores` threads.
+    Returns (Gbps, sample description, seconds)."""
+    import oracle
+    import synth
+    key = synth.key(KEYBITS)
+    probe = 4096 * max(1, cores)
+    buf = synth.blocks(0, probe)
+    t0 = time.perf_counter()
+    ct = oracle.encrypt(key, buf, nthreads=cores)
+    oracle.decrypt(key, ct, nthreads=cores)
+    dt = time.perf_counter() - t0
+    rate = 2 * buf.size / dt                       # payload B/s, enc+dec
+    nb = int(min(GIB, max(probe * 16, rate * target_s / 2)) // 16)
+    buf = synth.blocks(0, nb)
+    t0 = time.perf_counter()
+    ct = oracle.encrypt(key, buf, nthreads=cores)
+    oracle.decrypt(key, ct, nthreads=cores)
+    dt = time.perf_counter() - t0
+    gbps = 8 * 2 * buf.size / dt / 1e9
+    return gbps, f"first {nb} blocks ({buf.size / 2**20:.1f} MiB) of the bench stream, encrypt+decrypt", dt
+
+
+def run_reference(a):
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    if rank != 0:
+        return 0
+    cores = host_cores()
+    per_step = max(1.0, min(20.0, 150.0 / max(1, a.steps + a.warmup)))
+    for _ in range(a.warmup):
+        time_oracle(per_step / 4, cores)
+    vals, secs = [], 0.0
+    sample = ""
+    for _ in range(a.steps):
+        g, sample, dt = time_oracle(per_step, cores)
+        vals.append(g)
+        secs += dt
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "Gbps", "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * secs / a.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (splitmix64 stream, seed 190205234)",
+        "config": {"workload": WORKLOAD, "keybits": KEYBITS, "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "Gbps", "cores": cores, "kind": "oracle", "sample": sample,
+                         "cpu": cpu_model()},
+        "e2e": {"value": v, "unit": "Gbps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference arm = the plain byte-oriented CPU oracle (no reference code exists; DESIGN.md)",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
+        self.gpu = gpu_index
+        self.p = None
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in open(self.path):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); smax.append(float(f[2])); power.append(float(f[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(power)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", d
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)", {}
+
+
+def ncu_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(p):
+        try:
+            d = json.load(open(p))
+            return d.get("dominant_kernel_dram_bytes_per_launch"), d.get("source")
+        except Exception:
+            pass
+    return None, None
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(a):
+    import numpy as np
+    import torch
+
+    from paper_1902_05234_b200 import dist as pdist
+    rank, world, local = pdist.init()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    import paper_1902_05234_b200 as aes   # ImportError if libaes_b200.so is missing
+    import synth
+
+    nbytes = (a.bytes_per_gpu // 16) * 16
+    n = nbytes // 16
+    first = rank * n                      # this rank's slice of the global stream
+    key = synth.key(KEYBITS)
+    rk = aes.expand_key(key)
+
+    x = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    ct = torch.empty_like(x)
+    pt = torch.empty_like(x)
+    s = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(s):
+        synth.fill_device(x, first_block=first)
+    s.synchronize()
+
+    # ---- parity gate (no timing record without parity) -------
+    import oracle
+    with torch.cuda.stream(s):
+        aes.ecb_encrypt(rk, x, out=ct)
+        aes.ecb_decrypt(rk, ct, out=pt)
+    s.synchronize()
+    rng = np.random.default_rng(1234 + rank)
+    idx = np.unique(np.r_[0, 1, n // 2, n - 2, n - 1, rng.integers(0, n, 2048)]).astype(np.int64)
+    want = oracle.encrypt(key, synth.blocks_at((first + idx).astype(np.uint64)).reshape(-1), nthreads=host_cores())
+    got = ct.view(-1, 16)[torch.from_numpy(idx).to(dev)].cpu().numpy().reshape(-1)
+    ok = bool(np.array_equal(got, want)) and bool(torch.equal(pt, x))
+    bad = pdist.sum_over_ranks(0.0 if ok else 1.0, dev)
+    if bad:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "error": "parity failed; no timing recorded"}), flush=True)
+        return 1
+
+    # ---- LDS-gather ceiling, measured live (binding roofline) --------------
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    sink = torch.empty(nsm * 1024, dtype=torch.int32, device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        aes.lds_gather(sink, nsm, 64)
+        e0.record(s)
+        looks = aes.lds_gather(sink, nsm, 4096)
+        e1.record(s)
+    s.synchronize()
+    lds_peak = looks / (e0.elapsed_time(e1) * 1e-3)          # lookups / s
+
+    # ---- step ------------------------------------------------------------
+    def step(ev=None):
+        r = aes.expand_key(key)                               # A1/A2 (host)
+        if ev:
+            ev[0].record(s)
+        aes.ecb_encrypt(r, x, out=ct)
+        if ev:
+            ev[1].record(s)
+        aes.ecb_decrypt(r, ct, out=pt)
+        if ev:
+            ev[2].record(s)
+
+    with torch.cuda.stream(s):
+        for _ in range(a.warmup):
+            step()
+    s.synchronize()
+
+    K = a.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    pdist.barrier(dev)
+    torch.cuda.synchronize(dev)
+    with torch.cuda.stream(s):
+        t_start.record(s)
+        for k in range(K):
+            step(evs[k])
+        t_end.record(s)
+    s.synchronize()
+    torch.cuda.synchronize(dev)
+    pdist.barrier(dev)
+    clocks = clk.stop()
+    ms_local = t_start.elapsed_time(t_end)
+    ms = pdist.max_over_ranks(ms_local, dev)
+    enc_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    dec_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    total_payload = pdist.sum_over_ranks(2.0 * nbytes * K, dev)
+    gbps = 8 * total_payload / (ms * 1e-3) / 1e9
+
+    # sanity after the timed region: decrypt(encrypt(x)) == x still
+    assert torch.equal(pt, x)
+
+    # ---- e2e: same metric through the C ABI with HOST buffers ------------
+    e2e = None
+    if not a.no_e2e:
+        hx = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        hx.copy_(x.cpu())
+        hc = torch.empty_like(hx).pin_memory()
+        hp = torch.empty_like(hx).pin_memory()
+        pipe = aes.Pipeline(chunk_bytes=64 << 20, depth=4)
+        pipe.run(rk, hx, hc)
+        pipe.run(rk, hc, hp, decrypt=True)
+        KE = max(1, min(K, 5))
+        pdist.barrier(dev)
+        t0 = time.perf_counter()
+        for _ in range(KE):
+            r = aes.expand_key(key)
+            pipe.run(r, hx, hc)
+            pipe.run(r, hc, hp, decrypt=True)
+        dt = pdist.max_over_ranks(time.perf_counter() - t0, dev)
+        pipe.close()
+        assert torch.equal(hp, hx)
+        e2e = {"value": 8 * pdist.sum_over_ranks(2.0 * nbytes * KE, dev) / dt / 1e9, "unit": "Gbps",
+               "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": 2 * nbytes,
+               "steps": KE, "timing": "host perf_counter around synchronous aes_pipeline_run calls, max over ranks",
+               "path": "aes_pipeline_run: pinned host -> H2D -> kernel -> D2H, 64 MiB chunks x 4 streams"}
+
+    # ---- roofline of the dominant kernel ---------------------------------
+    peak, peak_src, peaks = measured_peaks()
+    kern_ms = max(enc_ms, dec_ms)
+    dom = "encrypt" if enc_ms >= dec_ms else "decrypt"
+    achieved = 32.0 * n / (kern_ms * 1e-3) / 1e9               # GB/s, 16 B read + 16 B written per block
+    traffic, traffic_src = ncu_traffic()
+    lookups = 16 * NR * n
+    sm_clk = clocks.get("sm_mhz") or 1965.0
+    lds_nominal = nsm * 32 * sm_clk * 1e6
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "kernel": f"ecb_kernel<10,{dom}> (aes_ecb_{dom})", "kernel_ms": kern_ms,
+            "peak_source": peak_src, "algorithmic_bytes_per_launch": 32 * n,
+            "traffic_source": traffic_src}
+    roof_lds = {"bound": "smem_lookup", "achieved": lookups / (kern_ms * 1e-3) / 1e12,
+                "peak": lds_peak / 1e12, "unit": "Tlookup/s",
+                "frac": (lookups / (kern_ms * 1e-3)) / lds_peak,
+                "peak_source": "aes_mb_lds_gather measured in this run (conflict-free 1-PRMT LDS gathers)",
+                "nominal_peak": lds_nominal / 1e12, "frac_of_nominal": (lookups / (kern_ms * 1e-3)) / lds_nominal,
+                "lookups_per_launch": lookups}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        cores = host_cores()
+        g, sample, _ = time_oracle(a.cpu_seconds, cores)
+        cpu = {"value": g, "unit": "Gbps", "cores": cores, "kind": "oracle", "sample": sample, "cpu": cpu_model()}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": gbps, "unit": "Gbps", "n_gpus": world, "steps": K, "warmup": a.warmup,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8", "data": "synthetic (splitmix64 counter stream, seed 190205234; random-init key)",
+            "config": {"workload": WORKLOAD, "keybits": KEYBITS, "bytes_per_gpu": nbytes,
+                       "global_bytes": nbytes * world, "parallelism": f"dp{world} (contiguous block shards)",
+                       "step": "expand_key + encrypt(1 GiB) + decrypt(1 GiB)",
+                       "l2": "inputs (1 GiB) larger than L2 (126 MB); no flush",
+                       "variant": "smem_repl, 1 state/thread, persistent grid"},
+            "GBps": gbps / 8, "enc_ms": enc_ms, "dec_ms": dec_ms,
+            "enc_Gbps": 8 * nbytes / (enc_ms * 1e-3) / 1e9, "dec_Gbps": 8 * nbytes / (dec_ms * 1e-3) / 1e9,
+            "hbm_frac_step": (32.0 * n * 2 * K / (ms_local * 1e-3) / 1e9) / peak,
+            "roofline": roof, "roofline_lds": roof_lds, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clocks, "gpu_launches": 2 * K, "gpu": torch.cuda.get_device_name(dev),
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    return run_ours(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

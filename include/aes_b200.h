@@ -1,0 +1,154 @@
+/*
+ * aes_b200.h -- C ABI of the B200 (sm_100a) AES-ECB library  libaes_b200.so
+ *
+ * The hot path of arXiv 1902.05234 ("one state per thread", T-box rounds):
+ * given a cipher key and a message P = P_1..P_n of 16-byte states, produce
+ * C_i = Cipher_K(P_i) for every i (ECB, Eq 1), and the inverse.
+ * Rounds are computed as the paper's T-table round (Eq 26, PAPER.md:423-427;
+ * tables Eqs 22-25), one state per thread (sec 4.1,
+ * PAPER.md:435-436).  Decryption uses the equivalent inverse cipher
+ * (FIPS-197 5.3.5; reading R12), keys of 128/192/256 bits (R4).
+ *
+ * Conventions (R7, R9, R21):
+ *  - A 16-byte block is a 4x4 state, byte r+4c = row r of column c.
+ *  - Column c is the little-endian uint32 word c of the block.
+ *  - Round-key words are little-endian memory-order words: for the key
+ *    00 01 02 03 ..., ek[0] == 0x03020100.
+ *
+ * Thread safety: every entry point is re-entrant; the library keeps no
+ * per-call global mutable state (a per-device launch-attribute cache is
+ * initialised once under a lock).  No CUDA or torch types appear here: a
+ * stream is passed as `void *` holding a cudaStream_t (NULL = legacy default).
+ *
+ * Errors: status codes only -- no exceptions cross the ABI, nothing aborts.
+ * Argument validation happens before any launch.  On error `out` is left
+ * unspecified (no partial-output guarantee: the GPU analogue of SPEC.md:491).
+ * Kernel faults surface at the caller's next synchronisation.
+ * There is NO CPU fallback: host pointers passed to the device entry points
+ * are rejected with AES_ENOTDEVICE.
+ */
+#ifndef AES_B200_H
+#define AES_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AES_B200_ABI_VERSION 1
+
+typedef enum {
+    AES_OK = 0,
+    AES_EKEYBITS = 1,   /* keybits not in {128, 192, 256}                        */
+    AES_ENR = 2,        /* nr not in {10,12,14}, or nr != rk->nr                  */
+    AES_ENULL = 3,      /* a required pointer is NULL                             */
+    AES_EALIGN = 4,     /* in/out not 16-byte aligned                             */
+    AES_EOVERLAP = 5,   /* in and out partially overlap (in == out is allowed)    */
+    AES_ERANGE = 6,     /* 16*nblocks overflows, or a config value out of range   */
+    AES_ENOTDEVICE = 7, /* in/out not device memory of the current device         */
+    AES_ECUDA = 8,      /* a CUDA runtime call failed; see aes_last_cuda_error()  */
+    AES_EVARIANT = 9    /* unknown kernel variant / states-per-thread             */
+} aes_status;
+
+/* Expanded key.  Plain old data, caller-owned, 488 bytes.
+ *  ek: FIPS-197 KeyExpansion ("1408 bits" for AES-128), 4*(nr+1)
+ *      words used; round key r = ek[4r .. 4r+3] ("round keys are sequentially
+ *      taken from the expanded key").
+ *  dk: equivalent-inverse schedule in application order:
+ *      dk[0..3] = ek[4nr..], dk[4r+j] = InvMixColumns(ek[4(nr-r)+j]) for
+ *      1 <= r <= nr-1, dk[4nr..] = ek[0..3]  (FIPS-197 5.3.5; R12). */
+typedef struct {
+    uint32_t ek[60];
+    uint32_t dk[60];
+    int32_t nr;       /* 10 | 12 | 14 */
+    int32_t keybits;  /* 128 | 192 | 256 */
+} aes_round_keys;
+
+/* aes_expand_key: host only, no CUDA calls.  key: keybits/8 bytes, read only
+ * during the call.  out: caller-owned, fully written on AES_OK.
+ * Errors: AES_ENULL, AES_EKEYBITS.  Steps A1 + A2 of SURVEY.md 8(a). */
+aes_status aes_expand_key(const uint8_t *key, int keybits, aes_round_keys *out);
+
+/* aes_ecb_encrypt / aes_ecb_decrypt: enqueue C_i = E_K(P_i) (resp. P_i =
+ * D_K(C_i)) for i < nblocks on `stream`, asynchronously.
+ *  rk      : host pointer, read during the call only (round keys are copied
+ *            by value into the kernel parameters -> constant bank, PAPER.md
+ *            sec 4.3 "round keys in the constant memory", 452-454).
+ *  nr      : must equal rk->nr (guards against a stale/mismatched schedule).
+ *  in, out : device pointers of the current device, 16-byte aligned,
+ *            16*nblocks bytes each; in == out (in place) is allowed, any
+ *            other overlap is AES_EOVERLAP.  Caller keeps them alive until the
+ *            stream work completes.
+ *  nblocks : number of 16-byte states (64-bit; > 2^32 supported).  0 -> AES_OK
+ *            without a launch.
+ *  stream  : cudaStream_t as void*, NULL = legacy default stream.
+ * Errors: AES_ENULL, AES_ENR, AES_EALIGN, AES_EOVERLAP, AES_ERANGE,
+ *         AES_ENOTDEVICE, AES_ECUDA.  Uses the tuned default kernel variant. */
+aes_status aes_ecb_encrypt(const aes_round_keys *rk, int nr, const void *in, void *out,
+                           uint64_t nblocks, void *stream);
+aes_status aes_ecb_decrypt(const aes_round_keys *rk, int nr, const void *in, void *out,
+                           uint64_t nblocks, void *stream);
+
+/* Kernel variants (T-table placement).  All variants
+ * produce bit-identical output; they differ only in speed.
+ *  AES_VAR_DEFAULT    : tuned choice (currently AES_VAR_SMEM_REPL).
+ *  AES_VAR_SMEM_REPL  : Te0..Te3 (Td0..Td3, Si) replicated 32x in shared
+ *                       memory, bank == lane, conflict-free by construction.
+ *  AES_VAR_SMEM_PLAIN : one copy of each table in shared memory (Li et al.,
+ *                       PAPER.md:41); data-dependent bank conflicts.
+ *  AES_VAR_CONST      : tables in __constant__ memory (the paper's choice,
+ *                       PAPER.md:443); serialises divergent addresses. */
+typedef enum {
+    AES_VAR_DEFAULT = 0,
+    AES_VAR_SMEM_REPL = 1,
+    AES_VAR_SMEM_PLAIN = 2,
+    AES_VAR_CONST = 3
+} aes_variant;
+
+typedef struct {
+    int32_t variant;           /* aes_variant                                      */
+    int32_t states_per_thread; /* 0 = default; else 1, 2 or 4 (granularity, 8(a) A10) */
+    int32_t grid;              /* 0 = persistent default (SMs x resident CTAs)     */
+    int32_t reserved;
+} aes_launch_config;
+
+/* Same contract as aes_ecb_encrypt/decrypt (decrypt = 0/1) with an explicit
+ * variant; cfg may be NULL (= defaults).  AES_EVARIANT for an unknown variant
+ * or states_per_thread value, AES_ERANGE for a negative grid. */
+aes_status aes_ecb_launch(const aes_round_keys *rk, int nr, int decrypt, const void *in,
+                          void *out, uint64_t nblocks, void *stream,
+                          const aes_launch_config *cfg);
+
+/* Host-resident end-to-end path (the paper's timing
+ * boundary, "we get back the encrypted data from GPU memory").
+ * A pipeline owns `depth` device staging buffers of chunk_bytes each and
+ * `depth` streams on the device that is current at creation.  Run copies host
+ * -> device, ciphers, and copies device -> host chunk by chunk, with the
+ * three stages of different chunks overlapped; it returns when out_host is
+ * complete (synchronous).  in_host/out_host: host memory, 16*nblocks bytes,
+ * ideally page-locked (pageable memory works but does not overlap);
+ * in_host == out_host allowed.  chunk_bytes: multiple of 16, >= 16; depth 1..8.
+ * Errors: AES_ENULL, AES_ERANGE, AES_ENR, AES_EOVERLAP, AES_ECUDA. */
+typedef struct aes_pipeline aes_pipeline;
+aes_status aes_pipeline_create(uint64_t chunk_bytes, int depth, aes_pipeline **out);
+aes_status aes_pipeline_run(aes_pipeline *p, const aes_round_keys *rk, int nr, int decrypt,
+                            const void *in_host, void *out_host, uint64_t nblocks);
+aes_status aes_pipeline_destroy(aes_pipeline *p);
+
+/* Shared-memory gather microbenchmark (the binding roofline):
+ * `grid` CTAs x 1024 threads each perform `iters` x 16 conflict-free 32-bit
+ * lookups into a lane-replicated 128 KiB table with the same one-PRMT address
+ * form as the AES rounds, on `stream`.  sink: device pointer, >= 4*grid*1024
+ * bytes, receives a checksum (keeps the loads live).  Time it with events. */
+aes_status aes_mb_lds_gather(void *sink, int grid, int iters, void *stream);
+
+const char *aes_status_string(aes_status s);
+/* cudaError_t (as int) behind the last AES_ECUDA returned on this thread. */
+int aes_last_cuda_error(void);
+int aes_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AES_B200_H */

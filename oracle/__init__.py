@@ -30,7 +30,7 @@ def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (plain C, -O2, pthreads)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread",
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-fno-semantic-interposition", "-shared", "-pthread",
                                "-o", tmp, _SRC])
         os.replace(tmp, _LIB)
     return _LIB

@@ -1,0 +1,187 @@
+"""B200 (sm_100a) AES-128/192/256 ECB -- thin Python binding over libaes_b200.so.
+
+The hot path of arXiv 1902.05234 (T-box rounds, one state per thread, ECB):
+    rk = expand_key(key)                      # aes_expand_key (host, C++)
+    ct = ecb_encrypt(rk, x)                   # aes_ecb_encrypt (CUDA kernel)
+    pt = ecb_decrypt(rk, ct)                  # aes_ecb_decrypt (CUDA kernel)
+``x`` is a contiguous torch.uint8 CUDA tensor whose length is a multiple of 16
+(padding is the caller's job, R17).  Work is enqueued on
+``torch.cuda.current_stream()``.  This module only marshals arguments; every
+step of the path runs in the library's kernels.  There is no CPU fallback:
+CPU tensors raise TypeError.
+"""
+from __future__ import annotations
+
+import ctypes
+
+from . import _native
+from ._native import (AES_VAR_CONST, AES_VAR_DEFAULT, AES_VAR_SMEM_PLAIN, AES_VAR_SMEM_REPL,
+                      aes_launch_config, aes_round_keys, status_string)
+
+__all__ = ["RoundKeys", "expand_key", "ecb_encrypt", "ecb_decrypt", "ecb", "Pipeline",
+           "lds_gather", "AesError", "AES_VAR_DEFAULT", "AES_VAR_SMEM_REPL", "AES_VAR_SMEM_PLAIN",
+           "AES_VAR_CONST", "abi_version"]
+
+
+class AesError(RuntimeError):
+    def __init__(self, code: int, what: str = ""):
+        self.code = code
+        msg = status_string(code)
+        if code == _native.AES_ECUDA:
+            msg += f" (cudaError {_native.lib.aes_last_cuda_error()})"
+        super().__init__(f"{what}: {msg}" if what else msg)
+
+
+def _check(code: int, what: str):
+    if code != _native.AES_OK:
+        raise AesError(code, what)
+
+
+class RoundKeys:
+    """Expanded key (aes_round_keys): ek, dk (equivalent inverse), nr, keybits."""
+
+    __slots__ = ("c",)
+
+    def __init__(self, c: aes_round_keys):
+        self.c = c
+
+    @property
+    def nr(self) -> int:
+        return self.c.nr
+
+    @property
+    def keybits(self) -> int:
+        return self.c.keybits
+
+    @property
+    def ek(self) -> list[int]:
+        return list(self.c.ek[: 4 * (self.nr + 1)])
+
+    @property
+    def dk(self) -> list[int]:
+        return list(self.c.dk[: 4 * (self.nr + 1)])
+
+
+def abi_version() -> int:
+    return _native.lib.aes_abi_version()
+
+
+def expand_key(key: bytes) -> RoundKeys:
+    """aes_expand_key: 16/24/32-byte key -> round keys (ValueError otherwise)."""
+    key = bytes(key)
+    if len(key) not in (16, 24, 32):
+        raise ValueError("AES key must be 16, 24 or 32 bytes")
+    rk = aes_round_keys()
+    _check(_native.lib.aes_expand_key(key, 8 * len(key), ctypes.byref(rk)), "aes_expand_key")
+    return RoundKeys(rk)
+
+
+def _check_tensor(x, name):
+    import torch
+    if not isinstance(x, torch.Tensor):
+        raise TypeError(f"{name} must be a torch tensor")
+    if not x.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if x.dtype != torch.uint8:
+        raise TypeError(f"{name} must be torch.uint8")
+    if not x.is_contiguous():
+        raise TypeError(f"{name} must be contiguous")
+    if x.numel() % 16:
+        raise ValueError(f"{name}.numel() must be a multiple of 16 (whole AES blocks)")
+
+
+def ecb(rk: RoundKeys, x, decrypt: bool, out=None, variant: int = AES_VAR_DEFAULT,
+        states_per_thread: int = 0, grid: int = 0, stream=None):
+    """ECB over a device buffer; ``out`` may be ``x`` (in place) or None (new tensor)."""
+    import torch
+    _check_tensor(x, "x")
+    if out is None:
+        out = torch.empty_like(x)
+    else:
+        _check_tensor(out, "out")
+        if out.numel() != x.numel():
+            raise ValueError("out must have the same size as x")
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    n = x.numel() // 16
+    with torch.cuda.device(x.device):
+        if variant == AES_VAR_DEFAULT and not states_per_thread and not grid:
+            fn = _native.lib.aes_ecb_decrypt if decrypt else _native.lib.aes_ecb_encrypt
+            code = fn(ctypes.byref(rk.c), rk.nr, ctypes.c_void_p(x.data_ptr()),
+                      ctypes.c_void_p(out.data_ptr()), n, ctypes.c_void_p(s.cuda_stream))
+        else:
+            cfg = aes_launch_config(variant, states_per_thread, grid, 0)
+            code = _native.lib.aes_ecb_launch(ctypes.byref(rk.c), rk.nr, int(bool(decrypt)),
+                                              ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                              n, ctypes.c_void_p(s.cuda_stream), ctypes.byref(cfg))
+    _check(code, "aes_ecb_decrypt" if decrypt else "aes_ecb_encrypt")
+    return out
+
+
+def ecb_encrypt(rk: RoundKeys, x, out=None, **kw):
+    return ecb(rk, x, False, out, **kw)
+
+
+def ecb_decrypt(rk: RoundKeys, x, out=None, **kw):
+    return ecb(rk, x, True, out, **kw)
+
+
+class Pipeline:
+    """Host-resident end-to-end path: aes_pipeline_create/run/destroy.
+
+    ``run`` takes host buffers (numpy arrays or CPU uint8 tensors, ideally
+    pinned), copies chunks to the device, ciphers them there and copies them
+    back, overlapping the three stages across ``depth`` streams.  Synchronous.
+    """
+
+    def __init__(self, chunk_bytes: int = 64 << 20, depth: int = 3, device=None):
+        import torch
+        self.h = ctypes.c_void_p()
+        dev = torch.cuda.current_device() if device is None else device
+        with torch.cuda.device(dev):
+            _check(_native.lib.aes_pipeline_create(chunk_bytes, depth, ctypes.byref(self.h)),
+                   "aes_pipeline_create")
+
+    @staticmethod
+    def _ptr_len(a):
+        import numpy as np
+        import torch
+        if isinstance(a, torch.Tensor):
+            if a.is_cuda or a.dtype != torch.uint8 or not a.is_contiguous():
+                raise TypeError("host buffers must be contiguous CPU uint8 tensors")
+            return a.data_ptr(), a.numel()
+        if isinstance(a, np.ndarray):
+            if a.dtype != np.uint8 or not a.flags["C_CONTIGUOUS"]:
+                raise TypeError("host buffers must be contiguous uint8 arrays")
+            return a.ctypes.data, a.size
+        raise TypeError("host buffer must be a numpy array or CPU tensor")
+
+    def run(self, rk: RoundKeys, src, dst, decrypt: bool = False):
+        ps, ns = self._ptr_len(src)
+        pd, nd = self._ptr_len(dst)
+        if ns != nd or ns % 16:
+            raise ValueError("src/dst must have equal sizes, a multiple of 16")
+        _check(_native.lib.aes_pipeline_run(self.h, ctypes.byref(rk.c), rk.nr, int(bool(decrypt)),
+                                            ctypes.c_void_p(ps), ctypes.c_void_p(pd), ns // 16),
+               "aes_pipeline_run")
+        return dst
+
+    def close(self):
+        if self.h:
+            _native.lib.aes_pipeline_destroy(self.h)
+            self.h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def lds_gather(sink, grid: int, iters: int, stream=None):
+    """Launch the shared-memory gather microbenchmark (aes_mb_lds_gather)."""
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream(sink.device)
+    with torch.cuda.device(sink.device):
+        _check(_native.lib.aes_mb_lds_gather(ctypes.c_void_p(sink.data_ptr()), grid, iters,
+                                             ctypes.c_void_p(s.cuda_stream)), "aes_mb_lds_gather")
+    return 16 * iters * grid * 1024  # lookups issued

@@ -1,0 +1,70 @@
+"""Multi-GPU plumbing for the ECB path.
+
+ECB blocks are independent (Eq 1; Table 1 "Suitable",
+PAPER.md:153,161), so a buffer of n blocks is split into N contiguous shards,
+one per rank/GPU, with NO collective on the data path.  torch.distributed is
+used only to start, align (barrier) and time the ranks (MAX of elapsed
+times, SUM of counts).  Works with the nccl backend on GPUs and gloo on CPU.
+"""
+from __future__ import annotations
+
+import os
+
+
+def shard_range(nblocks: int, rank: int, world: int) -> tuple[int, int]:
+    """Rank r of N owns global blocks [r*n//N, (r+1)*n//N)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return nblocks * rank // world, nblocks * (rank + 1) // world
+
+
+def env_rank_world() -> tuple[int, int, int]:
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def init(backend: str | None = None):
+    """Initialise the default process group from torchrun's env (if WORLD_SIZE>1)."""
+    import torch
+    import torch.distributed as dist
+    rank, world, local = env_rank_world()
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if backend is None:
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group(backend, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return rank, world, local
+
+
+def _reduce(value: float, op, device=None) -> float:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64,
+                     device=device if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=op)
+    return float(t.item())
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    import torch.distributed as dist
+    return _reduce(value, dist.ReduceOp.MAX, device)
+
+
+def sum_over_ranks(value: float, device=None) -> float:
+    import torch.distributed as dist
+    return _reduce(value, dist.ReduceOp.SUM, device)
+
+
+def barrier(device=None):
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        if dist.get_backend() == "nccl" and device is not None:
+            dist.barrier(device_ids=[device.index if hasattr(device, "index") else int(device)])
+        else:
+            dist.barrier()

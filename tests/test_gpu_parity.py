@@ -1,0 +1,212 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bit-exact, zero tolerance (integer work with a unique result, R23).
+Inputs are the seeded splitmix64 stream (synth/), the same bytes on both
+sides; expected values come only from oracle/.  Sizes span one warp, several
+CTAs and ragged tails; full BASELINE sizes are checked on sampled blocks the
+oracle computes one by one, plus an on-device round trip.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle
+import synth
+from conftest import golden
+
+VARIANTS = [(1, 1), (1, 2), (1, 4), (2, 1), (3, 1)]   # (variant, states_per_thread)
+SIZES = [1, 2, 31, 32, 33, 1023, 1024, 1025, 4096 + 17, 148 * 1024 + 7, 65536]
+
+
+@pytest.fixture(scope="module")
+def aes():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1902_05234_b200 as m
+    assert torch.cuda.is_available(), "GPU test on a box without CUDA"
+    return m
+
+
+def _dev_rand(n, first=0, kind="random"):
+    x = torch.empty(16 * n, dtype=torch.uint8, device="cuda")
+    synth.fill_device(x, first_block=first, kind=kind)
+    return x
+
+
+def test_device_generator_matches_host_twin(aes):
+    for first, n in ((0, 1000), (12345, 777)):
+        x = _dev_rand(n, first)
+        assert np.array_equal(x.cpu().numpy(), synth.blocks(first, n))
+    for kind in ("zeros", "repeat", "ascii"):
+        x = _dev_rand(300, 0, kind)
+        assert np.array_equal(x.cpu().numpy(), synth.blocks(0, 300, kind=kind))
+
+
+def test_fips197_and_sp800_38a_vectors_all_variants(aes):
+    rows = [ln.split() for ln in open(golden("fips197_appC.txt")) if ln.strip() and not ln.startswith("#")]
+    sp = [ln.split() for ln in open(golden("sp800_38a_ecb.txt")) if ln.strip() and not ln.startswith("#")]
+    pt4 = bytes.fromhex("".join(sp[0][1:]))
+    for i in range(1, 7, 2):
+        rows.append([sp[i][1], pt4.hex(), "".join(sp[i + 1][1:])])
+    for key, pt, ct in rows:
+        rk = aes.expand_key(bytes.fromhex(key))
+        x = torch.frombuffer(bytearray(bytes.fromhex(pt)), dtype=torch.uint8).cuda()
+        c = torch.frombuffer(bytearray(bytes.fromhex(ct)), dtype=torch.uint8).cuda()
+        for v, spt in VARIANTS:
+            got = aes.ecb_encrypt(rk, x, variant=v, states_per_thread=spt)
+            assert got.cpu().numpy().tobytes().hex() == ct, (key, v, spt)
+            back = aes.ecb_decrypt(rk, c, variant=v, states_per_thread=spt)
+            assert back.cpu().numpy().tobytes().hex() == pt, (key, v, spt)
+
+
+@pytest.mark.parametrize("keybits", [128, 192, 256])
+def test_random_buffers_against_oracle(aes, keybits):
+    key = synth.key(keybits)
+    rk = aes.expand_key(key)
+    for n in SIZES:
+        x = _dev_rand(n, first=n)
+        host = synth.blocks(n, n)
+        want_ct = oracle.encrypt(key, host, nthreads=8)
+        want_pt = oracle.decrypt(key, host, nthreads=8)   # decrypt of arbitrary input
+        for v, spt in VARIANTS:
+            ct = aes.ecb_encrypt(rk, x, variant=v, states_per_thread=spt).cpu().numpy()
+            assert np.array_equal(ct, want_ct), (keybits, n, v, spt, int(np.argmax(ct != want_ct)) // 16)
+            pt = aes.ecb_decrypt(rk, x, variant=v, states_per_thread=spt).cpu().numpy()
+            assert np.array_equal(pt, want_pt), (keybits, n, v, spt)
+
+
+def test_small_grids_many_trips_and_in_place(aes):
+    key = synth.key(128)
+    rk = aes.expand_key(key)
+    n = 3 * 1024 * 4 + 5
+    x = _dev_rand(n)
+    want = oracle.encrypt(key, synth.blocks(0, n), nthreads=8)
+    for grid in (1, 2, 3, 7):
+        for spt in (1, 2, 4):
+            ct = aes.ecb_encrypt(rk, x, grid=grid, variant=1, states_per_thread=spt)
+            assert np.array_equal(ct.cpu().numpy(), want), (grid, spt)
+    y = x.clone()
+    aes.ecb_encrypt(rk, y, out=y)
+    assert np.array_equal(y.cpu().numpy(), want)
+    aes.ecb_decrypt(rk, y, out=y)
+    assert torch.equal(y, x)
+
+
+def test_data_structure_variants(aes):
+    key = synth.key(128)
+    rk = aes.expand_key(key)
+    for kind in ("zeros", "repeat", "ascii"):
+        x = _dev_rand(5000, kind=kind)
+        want = oracle.encrypt(key, synth.blocks(0, 5000, kind=kind), nthreads=8)
+        assert np.array_equal(aes.ecb_encrypt(rk, x).cpu().numpy(), want), kind
+
+
+def test_empty_buffer_and_errors_on_device(aes):
+    from paper_1902_05234_b200 import _native
+    rk = aes.expand_key(bytes(16))
+    e = torch.empty(0, dtype=torch.uint8, device="cuda")
+    assert aes.ecb_encrypt(rk, e).numel() == 0
+    host = np.zeros(64, np.uint8)
+    code = _native.lib.aes_ecb_encrypt(ctypes.byref(rk.c), 10, ctypes.c_void_p(host.ctypes.data),
+                                       ctypes.c_void_p(host.ctypes.data), 4, None)
+    assert code == _native.AES_ENOTDEVICE
+    pinned = torch.zeros(64, dtype=torch.uint8).pin_memory()
+    code = _native.lib.aes_ecb_encrypt(ctypes.byref(rk.c), 10, ctypes.c_void_p(pinned.data_ptr()),
+                                       ctypes.c_void_p(pinned.data_ptr()), 4, None)
+    assert code == _native.AES_ENOTDEVICE
+    x = torch.zeros(64 + 8, dtype=torch.uint8, device="cuda")
+    with pytest.raises(aes.AesError):
+        aes.ecb_encrypt(rk, x[8:], out=torch.empty(64, dtype=torch.uint8, device="cuda"))
+
+
+def test_concurrent_streams_different_keys(aes):
+    n = 200000
+    x = _dev_rand(n)
+    host = synth.blocks(0, n)
+    outs = []
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    keys = [synth.key(128), synth.key(192), synth.key(256)]
+    torch.cuda.synchronize()
+    for s, k in zip(streams, keys):
+        with torch.cuda.stream(s):
+            outs.append(aes.ecb_encrypt(aes.expand_key(k), x))
+    torch.cuda.synchronize()
+    for o, k in zip(outs, keys):
+        sel = np.r_[0:64, n - 64:n]
+        want = oracle.encrypt(k, host.reshape(-1, 16)[sel].copy().reshape(-1))
+        assert np.array_equal(o.cpu().numpy().reshape(-1, 16)[sel].reshape(-1), want)
+
+
+def test_host_pipeline_end_to_end(aes):
+    key = synth.key(256)
+    rk = aes.expand_key(key)
+    n = 70001
+    host = synth.blocks(0, n)
+    src = torch.from_numpy(host.copy()).pin_memory()
+    dst = torch.empty_like(src).pin_memory()
+    p = aes.Pipeline(chunk_bytes=16 * 4099, depth=3)
+    p.run(rk, src, dst)
+    want = oracle.encrypt(key, host, nthreads=8)
+    assert np.array_equal(dst.numpy(), want)
+    p.run(rk, dst, dst, decrypt=True)   # in place
+    assert np.array_equal(dst.numpy(), host)
+    p.close()
+
+
+def _sample_idx(n, k=4096, seed=0):
+    rng = np.random.default_rng(seed)
+    edges = [0, 1, 2, n // 2 - 1, n // 2, n - 2, n - 1]
+    return np.unique(np.r_[edges, rng.integers(0, n, k)]).astype(np.int64)
+
+
+def test_config2_aes128_1gib_sampled_parity_and_round_trip(aes):
+    """BASELINE config 2 at full size: 1 GiB, AES-128, enc and dec, the
+    bench launch configuration (default variant, persistent grid)."""
+    n = (1 << 30) // 16
+    key = synth.key(128)
+    rk = aes.expand_key(key)
+    x = _dev_rand(n)
+    ct = aes.ecb_encrypt(rk, x)
+    back = aes.ecb_decrypt(rk, ct)
+    assert torch.equal(back, x)
+    idx = _sample_idx(n)
+    want = oracle.encrypt(key, synth.blocks_at(idx.astype(np.uint64)).reshape(-1), nthreads=8)
+    got = ct.view(-1, 16)[torch.from_numpy(idx).cuda()].cpu().numpy().reshape(-1)
+    assert np.array_equal(got, want)
+
+
+def test_config3_aes256_4gib_decrypt_sampled(aes):
+    """BASELINE config 3: AES-256 decrypt of a 4 GiB buffer (byte offsets
+    >= 2^32).  The ciphertext is the ORACLE's encryption at the sampled
+    blocks; the GPU decrypt must give back the generator's plaintext."""
+    free, _ = torch.cuda.mem_get_info()
+    if free < 10 * (1 << 30):
+        pytest.skip("needs ~10 GiB free")
+    n = (4 << 30) // 16
+    key = synth.key(256)
+    rk = aes.expand_key(key)
+    x = _dev_rand(n)
+    ct = aes.ecb_encrypt(rk, x)
+    idx = _sample_idx(n, seed=1)
+    idx = np.unique(np.r_[idx, (1 << 28) - 1, (1 << 28) - 2, ((1 << 32) // 16) - 1, (1 << 32) // 16])
+    idx = idx[idx < n]
+    sample_pt = synth.blocks_at(idx.astype(np.uint64)).reshape(-1)
+    sample_ct = oracle.encrypt(key, sample_pt, nthreads=8)
+    tidx = torch.from_numpy(idx).cuda()
+    assert np.array_equal(ct.view(-1, 16)[tidx].cpu().numpy().reshape(-1), sample_ct)
+    # overwrite the sampled blocks with the oracle's ciphertext, then GPU-decrypt all 4 GiB
+    ct.view(-1, 16)[tidx] = torch.from_numpy(sample_ct.reshape(-1, 16)).cuda()
+    pt = aes.ecb_decrypt(rk, ct, out=ct)
+    assert torch.equal(pt, x)
+    del x, ct
+
+
+def test_lds_gather_microbenchmark_runs(aes):
+    sink = torch.zeros(148 * 1024, dtype=torch.int32, device="cuda")
+    aes.lds_gather(sink, 148, 4)
+    torch.cuda.synchronize()
+    assert int(sink.abs().sum().item()) != 0
