@@ -1,0 +1,222 @@
+#!/usr/bin/env python
+"""Measurement sweeps beyond bench.py's headline line.
+
+  --what sizes     config 4: sizes 16 KiB .. 16 GiB x {128,192,256} x {enc,dec};
+                   fit t = t0 + n/R_inf per (keybits, dir) like the paper's Tables 4-5
+  --what variants  NEXT-2 ablation: table placement (replicated smem / plain smem /
+                   constant, the paper's choice) x states-per-thread, 1 GiB AES-128,
+                   plus data-structure variants (random / zeros / repeat / ascii)
+  --what config3   config 3: AES-256 decrypt, 4 GiB
+  --what ladder    the paper's file-size ladder (Tables 4-5), device-resident and e2e
+
+Every timed point is preceded by a parity check of that configuration against
+the oracle on sampled blocks.  Buffers smaller than 2x L2 are measured with an
+L2 flush (a 512 MiB write) before every rep; larger ones are not.  JSONL on stdout.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+import torch
+
+import oracle
+import paper_1902_05234_b200 as aes
+import synth
+
+NR = {128: 10, 192: 12, 256: 14}
+
+
+def peaks():
+    d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    return float(d["hbm_gbs"])
+
+
+def lds_peak(s):
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    sink = torch.empty(nsm * 1024, dtype=torch.int32, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        aes.lds_gather(sink, nsm, 64)
+        e0.record(s)
+        n = aes.lds_gather(sink, nsm, 4096)
+        e1.record(s)
+    s.synchronize()
+    return n / (e0.elapsed_time(e1) * 1e-3)
+
+
+def parity(key, x, out, decrypt, first=0, k=512):
+    n = x.numel() // 16
+    rng = np.random.default_rng(n)
+    idx = np.unique(np.r_[0, n - 1, rng.integers(0, n, k)]).astype(np.int64)
+    xin = x.view(-1, 16)[torch.from_numpy(idx).cuda()].cpu().numpy().reshape(-1)
+    want = oracle.ecb(key, xin, decrypt, nthreads=8)
+    got = out.view(-1, 16)[torch.from_numpy(idx).cuda()].cpu().numpy().reshape(-1)
+    if not np.array_equal(got, want):
+        raise SystemExit(f"PARITY FAILURE n={n} decrypt={decrypt}")
+
+
+def time_op(fn, s, reps, flush=None):
+    ts = []
+    for _ in range(reps):
+        if flush is not None:
+            flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record(s)
+            fn()
+            e1.record(s)
+        s.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e-3)
+    return min(ts), statistics.median(ts)
+
+
+def record(**kw):
+    print(json.dumps(kw), flush=True)
+
+
+def sizes(a, s, hbm, ldsp):
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    sz = [16 << 10, 64 << 10, 256 << 10, 1 << 20, 4 << 20, 16 << 20, 64 << 20, 256 << 20, 1 << 30, 4 << 30]
+    if a.big:
+        sz.append(16 << 30)
+    fits = {}
+    for nbytes in sz:
+        x = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        synth.fill_device(x)
+        out = torch.empty_like(x)
+        n = nbytes // 16
+        for kb in (128, 192, 256):
+            key = synth.key(kb)
+            rk = aes.expand_key(key)
+            for dec in (False, True):
+                f = (lambda: aes.ecb(rk, x, dec, out=out))
+                f()
+                torch.cuda.synchronize()
+                parity(key, x, out, dec)
+                reps = 20 if nbytes < (4 << 30) else 5
+                warm = nbytes >= 2 * l2
+                for _ in range(3):
+                    f()
+                tmin, tmed = time_op(f, s, reps, None if warm else flush)
+                g = 8 * nbytes / tmin / 1e9
+                fits.setdefault((kb, dec), []).append((n, tmin))
+                record(what="size", bytes=nbytes, keybits=kb, dir="dec" if dec else "enc", t_min_s=tmin,
+                       t_med_s=tmed, Gbps=g, GBps=g / 8, hbm_frac=32 * n / tmin / 1e9 / hbm,
+                       lds_frac=16 * NR[kb] * n / tmin / ldsp, l2="flushed" if not warm else "input>2xL2")
+        del x, out
+        torch.cuda.empty_cache()
+    for (kb, dec), pts in fits.items():
+        nn = np.array([p[0] for p in pts], float)
+        tt = np.array([p[1] for p in pts], float)
+        A = np.stack([np.ones_like(nn), nn], 1)
+        (t0, inv), *_ = np.linalg.lstsq(A, tt, rcond=None)
+        record(what="fit", keybits=kb, dir="dec" if dec else "enc", t0_us=t0 * 1e6,
+               R_inf_GBps=16 / inv / 1e9 if inv > 0 else None)
+
+
+def variants(a, s, hbm, ldsp):
+    nbytes = 1 << 30
+    x = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    out = torch.empty_like(x)
+    n = nbytes // 16
+    key = synth.key(128)
+    rk = aes.expand_key(key)
+    names = {1: "smem_repl", 2: "smem_plain", 3: "const (paper)"}
+    for kind in ("random", "zeros", "repeat", "ascii"):
+        synth.fill_device(x, kind=kind)
+        for v, spt in ((1, 1), (1, 2), (1, 4), (2, 1), (3, 1)):
+            if kind != "random" and v == 1 and spt != 1:
+                continue
+            for dec in (False, True):
+                f = (lambda: aes.ecb(rk, x, dec, out=out, variant=v, states_per_thread=spt))
+                f()
+                torch.cuda.synchronize()
+                parity(key, x, out, dec)
+                reps = 10 if v != 3 else 3
+                tmin, tmed = time_op(f, s, reps)
+                g = 8 * nbytes / tmin / 1e9
+                record(what="variant", variant=names[v], spt=spt, data=kind, dir="dec" if dec else "enc",
+                       keybits=128, bytes=nbytes, t_min_s=tmin, t_med_s=tmed, Gbps=g,
+                       hbm_frac=32 * n / tmin / 1e9 / hbm, lds_frac=160 * n / tmin / ldsp)
+
+
+def config3(a, s, hbm, ldsp):
+    nbytes = 4 << 30
+    x = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    synth.fill_device(x)
+    key = synth.key(256)
+    rk = aes.expand_key(key)
+    ct = aes.ecb_encrypt(rk, x)               # made outside the timed region
+    out = torch.empty_like(x)
+    f = (lambda: aes.ecb_decrypt(rk, ct, out=out))
+    f()
+    torch.cuda.synchronize()
+    assert torch.equal(out, x)
+    parity(key, ct, out, True)
+    for _ in range(3):
+        f()
+    tmin, tmed = time_op(f, s, 10)
+    n = nbytes // 16
+    g = 8 * nbytes / tmin / 1e9
+    record(what="config3", keybits=256, dir="dec", bytes=nbytes, t_min_s=tmin, t_med_s=tmed, Gbps=g,
+           hbm_frac=32 * n / tmin / 1e9 / hbm, lds_frac=224 * n / tmin / ldsp)
+
+
+def ladder(a, s, hbm, ldsp):
+    files = [1202, 4652, 9302, 18602, 37202, 74402, 148802, 297602, 595202, 1190402]
+    key = synth.key(128)
+    rk = aes.expand_key(key)
+    pipe = aes.Pipeline(chunk_bytes=1 << 20, depth=2)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    for fb in files:
+        nb = (fb + 15) // 16
+        x = torch.empty(16 * nb, dtype=torch.uint8, device="cuda")
+        synth.fill_device(x)
+        out = torch.empty_like(x)
+        hx = x.cpu().pin_memory()
+        ho = torch.empty_like(hx).pin_memory()
+        for dec in (False, True):
+            f = (lambda: aes.ecb(rk, x, dec, out=out))
+            f()
+            torch.cuda.synchronize()
+            parity(key, x, out, dec, k=64)
+            tmin, tmed = time_op(f, s, 20, flush)
+            import time
+            pipe.run(rk, hx, ho, decrypt=dec)
+            te = []
+            for _ in range(20):
+                t0 = time.perf_counter()
+                pipe.run(rk, hx, ho, decrypt=dec)
+                te.append(time.perf_counter() - t0)
+            assert np.array_equal(ho.numpy(), out.cpu().numpy())
+            record(what="ladder", file_bytes=fb, blocks=nb, dir="dec" if dec else "enc",
+                   kernel_t_min_s=tmin, kernel_Bps=fb / tmin, e2e_t_min_s=min(te), e2e_Bps=fb / min(te),
+                   paper_gpu_Bps=None)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--what", default="variants", choices=["sizes", "variants", "config3", "ladder", "all"])
+    ap.add_argument("--big", action="store_true", help="include 16 GiB in the size sweep")
+    a = ap.parse_args()
+    s = torch.cuda.Stream()
+    hbm = peaks()
+    ldsp = lds_peak(s)
+    record(what="peaks", hbm_gbs=hbm, lds_lookups_per_s=ldsp, gpu=torch.cuda.get_device_name(0))
+    todo = ["variants", "config3", "sizes", "ladder"] if a.what == "all" else [a.what]
+    for w in todo:
+        globals()[w](a, s, hbm, ldsp)
+
+
+if __name__ == "__main__":
+    main()
