@@ -90,6 +90,31 @@ aes_status aes_ecb_encrypt(const aes_round_keys *rk, int nr, const void *in, voi
 aes_status aes_ecb_decrypt(const aes_round_keys *rk, int nr, const void *in, void *out,
                            uint64_t nblocks, void *stream);
 
+/* aes_ctr_xcrypt: CTR mode (Eq 5,
+ * C_i = P_i xor CTR(R+i), "Suitable" for parallelism in Table 1), reading R24:
+ * the keystream block of block j (0-based) of this call is
+ * Cipher_K(iv + block_offset + j), the counter being the whole 16-byte block as
+ * a big-endian 128-bit integer, wrapping mod 2^128 (SP 800-38A 6.5 / B.1).
+ * Encryption and decryption are the same call.  block_offset lets a shard
+ * (rank r of a multi-GPU job) continue the global counter stream.
+ *  iv : host pointer to 16 bytes (initial counter block T_1), read during the call.
+ *  in/out/nblocks/stream : as aes_ecb_encrypt (in == out allowed).
+ * Errors: as aes_ecb_encrypt, plus AES_ENULL for iv. */
+aes_status aes_ctr_xcrypt(const aes_round_keys *rk, int nr, const uint8_t *iv, uint64_t block_offset,
+                          const void *in, void *out, uint64_t nblocks, void *stream);
+
+/* aes_cbc_decrypt: CBC decryption (Eq 2,
+ * printed without the cipher call -- reading R25: C_i = Cipher_K(P_i xor
+ * C_{i-1}), C_0 = IV), P_i = InvCipher_K(C_i) xor C_{i-1}.  Decryption is
+ * parallel (every C_{i-1} is already known); CBC ENCRYPTION is a sequential
+ * chain ("Unsuitable", Table 1) and is not offered.
+ *  iv : host pointer to 16 bytes, the block preceding in[0] (the IV for the
+ *       first shard, the last ciphertext block of the previous shard otherwise).
+ *  in == out is NOT allowed (AES_EOVERLAP): block i reads C_{i-1} after block
+ *  i-1 may have been overwritten.  Otherwise as aes_ecb_decrypt. */
+aes_status aes_cbc_decrypt(const aes_round_keys *rk, int nr, const uint8_t *iv, const void *in, void *out,
+                           uint64_t nblocks, void *stream);
+
 /* Kernel variants (T-table placement).  All variants
  * produce bit-identical output; they differ only in speed.
  *  AES_VAR_DEFAULT    : tuned choice (currently AES_VAR_SMEM_REPL).

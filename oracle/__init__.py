@@ -144,3 +144,47 @@ def encrypt(key: bytes, data, nthreads: int = 1) -> np.ndarray:
 
 def decrypt(key: bytes, data, nthreads: int = 1) -> np.ndarray:
     return ecb(key, data, True, nthreads)
+
+
+# --- CTR / CBC (NEXT-1 / NEXT-4) -------------------------------------------
+def _lib_modes():
+    L = lib()
+    if not getattr(L, "_modes", False):
+        p, i32, u64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_uint64
+        L.oracle_aes_ctr.restype = i32
+        L.oracle_aes_ctr.argtypes = [p, i32, p, u64, p, p, u64, i32]
+        L.oracle_aes_cbc.restype = i32
+        L.oracle_aes_cbc.argtypes = [p, i32, p, i32, p, p, u64]
+        L._modes = True
+    return L
+
+
+def _arr(data):
+    arr = np.frombuffer(data, dtype=np.uint8) if isinstance(data, (bytes, bytearray)) else data
+    if arr.dtype != np.uint8 or not arr.flags["C_CONTIGUOUS"] or arr.size % 16:
+        raise ValueError("need a contiguous uint8 buffer of whole blocks")
+    return arr
+
+
+def ctr(key: bytes, iv: bytes, data, block_offset: int = 0, nthreads: int = 1) -> np.ndarray:
+    """CTR (Eq 5, reading R24): block j uses counter iv + block_offset + j (BE, mod 2^128)."""
+    arr = _arr(data)
+    out = np.empty_like(arr)
+    assert len(iv) == 16
+    rc = _lib_modes().oracle_aes_ctr(_buf(key), 8 * len(key), _buf(iv), block_offset & (2**64 - 1),
+                                     arr.ctypes.data, out.ctypes.data, arr.size // 16, nthreads)
+    if rc:
+        raise ValueError("bad key size")
+    return out
+
+
+def cbc(key: bytes, iv: bytes, data, decrypt: bool) -> np.ndarray:
+    """CBC (Eq 2, reading R25), sequential."""
+    arr = _arr(data)
+    out = np.empty_like(arr)
+    assert len(iv) == 16
+    rc = _lib_modes().oracle_aes_cbc(_buf(key), 8 * len(key), _buf(iv), int(bool(decrypt)),
+                                     arr.ctypes.data, out.ctypes.data, arr.size // 16)
+    if rc:
+        raise ValueError("bad key size")
+    return out

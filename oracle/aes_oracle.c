@@ -343,3 +343,93 @@ int oracle_transform(int op, uint8_t blk[16]) {
     store_state(blk, &st);
     return 0;
 }
+
+/* ------------------------------------------------------------------------- */
+/* CTR and CBC (NEXT-1 / NEXT-4 of SURVEY.md 8(f))                            */
+/* ------------------------------------------------------------------------- */
+
+/* CTR, Eq 5: C_i = P_i xor CTR(R+i).  Reading R24: CTR(.)
+ * is Cipher_K of the counter block, the counter is the whole 16-byte block read
+ * as a big-endian 128-bit integer and incremented by one per block mod 2^128
+ * (SP 800-38A 6.5, B.1).  Block j (0-based, j >= 0) of this call uses counter
+ * iv + block_offset + j.  Encryption and decryption are the same operation. */
+static void counter_add(uint8_t ctr[16], uint64_t add) {
+    /* big-endian 128-bit add, carry propagated byte by byte */
+    unsigned carry = 0;
+    for (int b = 15; b >= 0; b--) {
+        unsigned v = ctr[b] + (unsigned)(add & 0xFF) + carry;
+        ctr[b] = (uint8_t)v;
+        carry = v >> 8;
+        add >>= 8;
+    }
+}
+
+typedef struct {
+    const uint8_t *in; uint8_t *out; const uint8_t *w; int nr;
+    uint8_t iv[16]; uint64_t off; uint64_t b0, b1;
+} ctr_job_t;
+
+static void *ctr_worker(void *arg) {
+    ctr_job_t *j = (ctr_job_t *)arg;
+    for (uint64_t b = j->b0; b < j->b1; b++) {
+        uint8_t ctr[16], ks[16];
+        memcpy(ctr, j->iv, 16);
+        counter_add(ctr, j->off);
+        counter_add(ctr, b);
+        cipher_block(ctr, ks, j->w, j->nr, NULL);
+        for (int k = 0; k < 16; k++) j->out[16 * b + k] = (uint8_t)(j->in[16 * b + k] ^ ks[k]);
+    }
+    return NULL;
+}
+
+int oracle_aes_ctr(const uint8_t *key, int keybits, const uint8_t iv[16], uint64_t block_offset,
+                   const uint8_t *in, uint8_t *out, uint64_t nblocks, int nthreads) {
+    uint8_t w[16 * 15];
+    int nr = oracle_key_expansion(key, keybits, w);
+    if (nr <= 0) return -1;
+    if (nblocks == 0) return 0;
+    if (nthreads < 1) nthreads = 1;
+    if ((uint64_t)nthreads > nblocks) nthreads = (int)nblocks;
+    if (nthreads > 1024) nthreads = 1024;
+    pthread_t tid[1024];
+    ctr_job_t jobs[1024];
+    for (int t = 0; t < nthreads; t++) {
+        jobs[t].in = in; jobs[t].out = out; jobs[t].w = w; jobs[t].nr = nr;
+        memcpy(jobs[t].iv, iv, 16); jobs[t].off = block_offset;
+        jobs[t].b0 = nblocks * (uint64_t)t / (uint64_t)nthreads;
+        jobs[t].b1 = nblocks * (uint64_t)(t + 1) / (uint64_t)nthreads;
+    }
+    if (nthreads == 1) { ctr_worker(&jobs[0]); return 0; }
+    for (int t = 0; t < nthreads; t++)
+        if (pthread_create(&tid[t], NULL, ctr_worker, &jobs[t]) != 0) { ctr_worker(&jobs[t]); tid[t] = 0; }
+    for (int t = 0; t < nthreads; t++) if (tid[t]) pthread_join(tid[t], NULL);
+    return 0;
+}
+
+/* CBC, Eq 2, printed as C_i = P_i xor C_{i-1} without the
+ * cipher call.  Reading R25: C_i = Cipher_K(P_i xor C_{i-1}), C_0 = IV
+ * (SP 800-38A 6.2); decryption P_i = InvCipher_K(C_i) xor C_{i-1}.
+ * Sequential, single-threaded, exactly as the equations read.  in == out is
+ * allowed (each C_{i-1} is saved before block i is overwritten). */
+int oracle_aes_cbc(const uint8_t *key, int keybits, const uint8_t iv[16], int decrypt,
+                   const uint8_t *in, uint8_t *out, uint64_t nblocks) {
+    uint8_t w[16 * 15];
+    int nr = oracle_key_expansion(key, keybits, w);
+    if (nr <= 0) return -1;
+    uint8_t prev[16];
+    memcpy(prev, iv, 16);
+    for (uint64_t b = 0; b < nblocks; b++) {
+        uint8_t x[16], y[16];
+        memcpy(x, in + 16 * b, 16);
+        if (!decrypt) {
+            for (int k = 0; k < 16; k++) y[k] = (uint8_t)(x[k] ^ prev[k]);
+            cipher_block(y, out + 16 * b, w, nr, NULL);
+            memcpy(prev, out + 16 * b, 16);
+        } else {
+            inv_cipher_block(x, y, w, nr);
+            for (int k = 0; k < 16; k++) out[16 * b + k] = (uint8_t)(y[k] ^ prev[k]);
+            memcpy(prev, x, 16);
+        }
+    }
+    return 0;
+}

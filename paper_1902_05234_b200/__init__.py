@@ -18,7 +18,7 @@ from . import _native
 from ._native import (AES_VAR_CONST, AES_VAR_DEFAULT, AES_VAR_SMEM_PLAIN, AES_VAR_SMEM_REPL,
                       aes_launch_config, aes_round_keys, status_string)
 
-__all__ = ["RoundKeys", "expand_key", "ecb_encrypt", "ecb_decrypt", "ecb", "Pipeline",
+__all__ = ["RoundKeys", "expand_key", "ecb_encrypt", "ecb_decrypt", "ecb", "ctr_xcrypt", "cbc_decrypt", "Pipeline",
            "lds_gather", "AesError", "AES_VAR_DEFAULT", "AES_VAR_SMEM_REPL", "AES_VAR_SMEM_PLAIN",
            "AES_VAR_CONST", "abi_version"]
 
@@ -123,6 +123,49 @@ def ecb_encrypt(rk: RoundKeys, x, out=None, **kw):
 
 def ecb_decrypt(rk: RoundKeys, x, out=None, **kw):
     return ecb(rk, x, True, out, **kw)
+
+
+def _prep_out(x, out):
+    import torch
+    _check_tensor(x, "x")
+    if out is None:
+        return torch.empty_like(x)
+    _check_tensor(out, "out")
+    if out.numel() != x.numel():
+        raise ValueError("out must have the same size as x")
+    return out
+
+
+def ctr_xcrypt(rk: RoundKeys, iv: bytes, x, out=None, block_offset: int = 0, stream=None):
+    """CTR (Eq 5, reading R24): out_j = x_j ^ E(iv + block_offset + j); iv = 16-byte BE counter."""
+    import torch
+    iv = bytes(iv)
+    if len(iv) != 16:
+        raise ValueError("iv must be 16 bytes")
+    out = _prep_out(x, out)
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    with torch.cuda.device(x.device):
+        code = _native.lib.aes_ctr_xcrypt(ctypes.byref(rk.c), rk.nr, iv, block_offset & (2**64 - 1),
+                                          ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                          x.numel() // 16, ctypes.c_void_p(s.cuda_stream))
+    _check(code, "aes_ctr_xcrypt")
+    return out
+
+
+def cbc_decrypt(rk: RoundKeys, iv: bytes, x, out=None, stream=None):
+    """CBC decryption (Eq 2, reading R25): out_i = D(x_i) ^ x_{i-1}, x_{-1} = iv.  Not in place."""
+    import torch
+    iv = bytes(iv)
+    if len(iv) != 16:
+        raise ValueError("iv must be 16 bytes")
+    out = _prep_out(x, out)
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    with torch.cuda.device(x.device):
+        code = _native.lib.aes_cbc_decrypt(ctypes.byref(rk.c), rk.nr, iv, ctypes.c_void_p(x.data_ptr()),
+                                           ctypes.c_void_p(out.data_ptr()), x.numel() // 16,
+                                           ctypes.c_void_p(s.cuda_stream))
+    _check(code, "aes_cbc_decrypt")
+    return out
 
 
 class Pipeline:

@@ -220,25 +220,79 @@ __device__ __forceinline__ uint4 cipher_block(const TB& tb, uint4 v, const RK& r
 }
 
 // ---------------------------------------------------------------------------
-// The ECB kernel: persistent grid-stride, SPT states per thread per trip
+// Kernels: persistent grid-stride, SPT states per thread per trip.
+//   ecb_kernel          C_i = E(P_i) / P_i = D(C_i)                (Eq 1)
+//   ctr_kernel          C_i = P_i ^ E(ctr0 + i), BE 128-bit counter  (Eq 5, R24)
+//   cbc_decrypt_kernel  P_i = D(C_i) ^ C_{i-1}, C_{-1} = IV          (Eq 2, R25)
 // ---------------------------------------------------------------------------
-template <int NR, bool DEC, int V, int SPT>
-__global__ void __launch_bounds__(kThreads, 1)
-    ecb_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n, const __grid_constant__ RK rk) {
+enum { M_ECB = 0, M_CTR = 1, M_CBCD = 2 };
+
+struct ModeP {
+    uint32_t iv[4];    // CBC: IV as LE column words
+    uint64_t ctr_hi;   // CTR: counter of block 0 of this launch, big-endian value,
+    uint64_t ctr_lo;   //      split into high / low 64 bits
+};
+
+__device__ __forceinline__ uint4 counter_block(const ModeP& mp, uint64_t i) {
+    uint64_t lo = mp.ctr_lo + i;
+    uint64_t hi = mp.ctr_hi + (lo < mp.ctr_lo ? 1ull : 0ull);   // carry, wraps mod 2^128
+    // block bytes 0..7 = hi big-endian, 8..15 = lo big-endian; columns are LE words
+    return make_uint4(__byte_perm((uint32_t)(hi >> 32), 0, 0x0123), __byte_perm((uint32_t)hi, 0, 0x0123),
+                      __byte_perm((uint32_t)(lo >> 32), 0, 0x0123), __byte_perm((uint32_t)lo, 0, 0x0123));
+}
+
+__device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
+    return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w);
+}
+
+template <int NR, bool DEC, int V, int SPT, int MODE>
+__device__ __forceinline__ void aes_body(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n,
+                                         const RK& rk, const ModeP& mp) {
     extern __shared__ __align__(16) uint32_t smem[];
     const Tab<V> tb = Tab<V>::template setup<DEC>(smem);   // A4
     const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += SPT * T) {
-        uint4 v[SPT];
+        uint4 v[SPT], w[SPT];
 #pragma unroll
-        for (int k = 0; k < SPT; k++)
-            if (i + k * T < n) v[k] = __ldcs(in + i + k * T);            // A5
+        for (int k = 0; k < SPT; k++) {
+            const uint64_t j = i + k * T;
+            if (j < n) {                                                   // A5
+                if (MODE == M_ECB) v[k] = __ldcs(in + j);
+                if (MODE == M_CTR) { v[k] = counter_block(mp, j); w[k] = __ldcs(in + j); }
+                if (MODE == M_CBCD) {
+                    v[k] = __ldg(in + j);
+                    w[k] = j ? __ldg(in + j - 1) : make_uint4(mp.iv[0], mp.iv[1], mp.iv[2], mp.iv[3]);
+                }
+            }
+        }
 #pragma unroll
         for (int k = 0; k < SPT; k++) v[k] = cipher_block<NR, DEC>(tb, v[k], rk);   // A6-A8
 #pragma unroll
-        for (int k = 0; k < SPT; k++)
-            if (i + k * T < n) __stcs(out + i + k * T, v[k]);             // A9
+        for (int k = 0; k < SPT; k++) {
+            const uint64_t j = i + k * T;
+            if (j < n) __stcs(out + j, MODE == M_ECB ? v[k] : xor4(v[k], w[k]));   // A9
+        }
     }
+}
+
+template <int NR, bool DEC, int V, int SPT>
+__global__ void __launch_bounds__(kThreads, 1)
+    ecb_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n, const __grid_constant__ RK rk) {
+    aes_body<NR, DEC, V, SPT, M_ECB>(in, out, n, rk, ModeP{});
+}
+
+template <int NR>
+__global__ void __launch_bounds__(kThreads, 1)
+    ctr_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n, const __grid_constant__ RK rk,
+               const __grid_constant__ ModeP mp) {
+    aes_body<NR, false, V_REPL, 1, M_CTR>(in, out, n, rk, mp);
+}
+
+template <int NR>
+__global__ void __launch_bounds__(kThreads, 1)
+    cbc_decrypt_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n,
+                       const __grid_constant__ RK rk, const __grid_constant__ ModeP mp) {
+    aes_body<NR, true, V_REPL, 1, M_CBCD>(in, out, n, rk, mp);
 }
 
 // ---------------------------------------------------------------------------
@@ -305,6 +359,18 @@ KernelInfo pick(int nr, bool dec, int v, int spt) {
         case 14: return dec ? pick_spt<14, true>(v, spt) : pick_spt<14, false>(v, spt);
     }
     return {nullptr, 0};
+}
+
+KernelInfo pick_mode(int nr, int mode) {
+    const void* f = nullptr;
+    if (mode == M_CTR) {
+        f = nr == 10 ? (const void*)&ctr_kernel<10> : nr == 12 ? (const void*)&ctr_kernel<12>
+                                                               : (const void*)&ctr_kernel<14>;
+        return {f, kSmemReplEnc};
+    }
+    f = nr == 10 ? (const void*)&cbc_decrypt_kernel<10> : nr == 12 ? (const void*)&cbc_decrypt_kernel<12>
+                                                                   : (const void*)&cbc_decrypt_kernel<14>;
+    return {f, kSmemReplDec};
 }
 
 thread_local int t_last_cuda_error = 0;
@@ -382,7 +448,8 @@ aes_status check_device_ptr(const void* p, int dev) {
 }
 
 aes_status launch(const aes_round_keys* rk, int nr, int decrypt, const void* in, void* out, uint64_t nblocks,
-                  cudaStream_t stream, const aes_launch_config* cfg, bool check_ptrs) {
+                  cudaStream_t stream, const aes_launch_config* cfg, bool check_ptrs, int mode = M_ECB,
+                  const ModeP* mp = nullptr) {
     aes_status st = validate_keys(rk, nr);
     if (st) return st;
     int variant = cfg ? cfg->variant : AES_VAR_DEFAULT;
@@ -391,10 +458,12 @@ aes_status launch(const aes_round_keys* rk, int nr, int decrypt, const void* in,
     if (variant == AES_VAR_DEFAULT) variant = V_REPL;
     if (spt == 0) spt = (variant == V_REPL) ? 1 : 1;
     if (grid_req < 0) return AES_ERANGE;
-    KernelInfo ki = pick(nr, decrypt != 0, variant, spt);
+    KernelInfo ki = mode == M_ECB ? pick(nr, decrypt != 0, variant, spt) : pick_mode(nr, mode);
+    if (mode != M_ECB) spt = 1;
     if (!ki.fn) return AES_EVARIANT;
     if (nblocks == 0) return AES_OK;
     if ((st = validate_buffers(in, out, nblocks))) return st;
+    if (mode == M_CBCD && in == out) return AES_EOVERLAP;   // C_{i-1} must survive block i-1's write
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e);
@@ -412,7 +481,8 @@ aes_status launch(const aes_round_keys* rk, int nr, int decrypt, const void* in,
     std::memcpy(k.w, decrypt ? rk->dk : rk->ek, sizeof k.w);
     const uint4* pin = static_cast<const uint4*>(in);
     uint4* pout = static_cast<uint4*>(out);
-    void* args[] = {(void*)&pin, (void*)&pout, (void*)&nblocks, (void*)&k};
+    ModeP m = mp ? *mp : ModeP{};
+    void* args[] = {(void*)&pin, (void*)&pout, (void*)&nblocks, (void*)&k, (void*)&m};
     e = cudaLaunchKernel(ki.fn, dim3(grid), dim3(kThreads), args, ki.smem, stream);
     if (e != cudaSuccess) return cuda_fail(e);
     return AES_OK;
@@ -437,6 +507,33 @@ aes_status aes_ecb_decrypt(const aes_round_keys* rk, int nr, const void* in, voi
 aes_status aes_ecb_launch(const aes_round_keys* rk, int nr, int decrypt, const void* in, void* out,
                           uint64_t nblocks, void* stream, const aes_launch_config* cfg) {
     return launch(rk, nr, decrypt, in, out, nblocks, (cudaStream_t)stream, cfg, true);
+}
+
+aes_status aes_ctr_xcrypt(const aes_round_keys* rk, int nr, const uint8_t* iv, uint64_t block_offset,
+                          const void* in, void* out, uint64_t nblocks, void* stream) {
+    aes_status st = validate_keys(rk, nr);
+    if (st) return st;
+    if (!iv) return AES_ENULL;
+    ModeP m{};
+    uint64_t hi = 0, lo = 0;
+    for (int b = 0; b < 8; b++) hi = (hi << 8) | iv[b];
+    for (int b = 8; b < 16; b++) lo = (lo << 8) | iv[b];
+    uint64_t lo2 = lo + block_offset;
+    m.ctr_hi = hi + (lo2 < lo ? 1 : 0);
+    m.ctr_lo = lo2;
+    return launch(rk, nr, 0, in, out, nblocks, (cudaStream_t)stream, nullptr, true, M_CTR, &m);
+}
+
+aes_status aes_cbc_decrypt(const aes_round_keys* rk, int nr, const uint8_t* iv, const void* in, void* out,
+                           uint64_t nblocks, void* stream) {
+    aes_status st = validate_keys(rk, nr);
+    if (st) return st;
+    if (!iv) return AES_ENULL;
+    ModeP m{};
+    for (int j = 0; j < 4; j++)
+        m.iv[j] = (uint32_t)iv[4 * j] | ((uint32_t)iv[4 * j + 1] << 8) | ((uint32_t)iv[4 * j + 2] << 16) |
+                  ((uint32_t)iv[4 * j + 3] << 24);
+    return launch(rk, nr, 1, in, out, nblocks, (cudaStream_t)stream, nullptr, true, M_CBCD, &m);
 }
 
 aes_status aes_mb_lds_gather(void* sink, int grid, int iters, void* stream) {

@@ -155,3 +155,19 @@ def test_python_layer_rejects_cpu_tensors():
         aes.ecb_encrypt(rk, torch.zeros(32, dtype=torch.uint8))
     with pytest.raises(TypeError):
         aes.ecb_encrypt(rk, np.zeros(32, np.uint8))
+
+
+def test_ctr_cbc_validation_errors():
+    from paper_1902_05234_b200 import _native
+    import paper_1902_05234_b200 as aes
+    rk = aes.expand_key(bytes(32))
+    L = _native.lib
+    A = 0x10000
+    iv = bytes(16)
+    assert L.aes_ctr_xcrypt(ctypes.byref(rk.c), 14, None, 0, A, A, 4, None) == _native.AES_ENULL
+    assert L.aes_ctr_xcrypt(ctypes.byref(rk.c), 10, iv, 0, A, A, 4, None) == _native.AES_ENR
+    assert L.aes_ctr_xcrypt(ctypes.byref(rk.c), 14, iv, 0, A, A, 0, None) == _native.AES_OK
+    assert L.aes_ctr_xcrypt(ctypes.byref(rk.c), 14, iv, 0, A, A + 32, 4, None) == _native.AES_EOVERLAP
+    assert L.aes_cbc_decrypt(ctypes.byref(rk.c), 14, None, A, A + 4096, 4, None) == _native.AES_ENULL
+    assert L.aes_cbc_decrypt(ctypes.byref(rk.c), 14, iv, A, A, 4, None) == _native.AES_EOVERLAP
+    assert L.aes_cbc_decrypt(ctypes.byref(rk.c), 14, iv, A + 4, A + 4096, 4, None) == _native.AES_EALIGN

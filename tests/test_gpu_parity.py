@@ -210,3 +210,66 @@ def test_lds_gather_microbenchmark_runs(aes):
     aes.lds_gather(sink, 148, 4)
     torch.cuda.synchronize()
     assert int(sink.abs().sum().item()) != 0
+
+
+# ---------------------------------------------------------------------------
+# NEXT-1 CTR and NEXT-4 CBC decryption
+# ---------------------------------------------------------------------------
+def _modes_golden():
+    rows = [ln.split() for ln in open(golden("sp800_38a_ctr_cbc.txt")) if ln.strip() and not ln.startswith("#")]
+    sp = [ln.split() for ln in open(golden("sp800_38a_ecb.txt")) if ln.strip() and not ln.startswith("#")]
+    pt = bytes.fromhex("".join(sp[0][1:]))
+    sets = [(bytes.fromhex(rows[i][1]), bytes.fromhex("".join(rows[i + 1][1:])),
+             bytes.fromhex("".join(rows[i + 2][1:]))) for i in range(2, len(rows), 3)]
+    return bytes.fromhex(rows[0][1]), bytes.fromhex(rows[1][1]), pt, sets
+
+
+def test_ctr_cbc_sp800_38a_vectors(aes):
+    ctr_iv, cbc_iv, pt, sets = _modes_golden()
+    tp = torch.frombuffer(bytearray(pt), dtype=torch.uint8).cuda()
+    for key, ctr_ct, cbc_ct in sets:
+        rk = aes.expand_key(key)
+        assert aes.ctr_xcrypt(rk, ctr_iv, tp).cpu().numpy().tobytes() == ctr_ct
+        tc = torch.frombuffer(bytearray(cbc_ct), dtype=torch.uint8).cuda()
+        assert aes.cbc_decrypt(rk, cbc_iv, tc).cpu().numpy().tobytes() == pt
+
+
+@pytest.mark.parametrize("keybits", [128, 192, 256])
+def test_ctr_random_against_oracle_wrap_and_offsets(aes, keybits):
+    key = synth.key(keybits)
+    rk = aes.expand_key(key)
+    rng = np.random.default_rng(keybits)
+    ivs = [bytes([0xFF] * 16), bytes(8) + bytes([0xFF] * 8), rng.integers(0, 256, 16, dtype=np.uint8).tobytes()]
+    for n in (1, 33, 1025, 148 * 1024 + 7):
+        x = _dev_rand(n, first=7 * n)
+        host = synth.blocks(7 * n, n)
+        for iv in ivs:
+            for off in (0, 12345, 2**64 - 3):
+                got = aes.ctr_xcrypt(rk, iv, x, block_offset=off).cpu().numpy()
+                assert np.array_equal(got, oracle.ctr(key, iv, host, block_offset=off, nthreads=8)), (n, iv.hex(), off)
+    # in place round trip
+    x = _dev_rand(5000)
+    y = x.clone()
+    aes.ctr_xcrypt(rk, ivs[2], y, out=y)
+    aes.ctr_xcrypt(rk, ivs[2], y, out=y)
+    assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("keybits", [128, 256])
+def test_cbc_decrypt_against_oracle_and_sharding(aes, keybits):
+    key = synth.key(keybits)
+    rk = aes.expand_key(key)
+    iv = bytes(range(16))
+    for n in (1, 2, 33, 1025, 148 * 1024 + 7):
+        pt = synth.blocks(0, n)
+        ct = oracle.cbc(key, iv, pt, decrypt=False)            # sequential oracle encryption
+        tc = torch.from_numpy(ct.copy()).cuda()
+        got = aes.cbc_decrypt(rk, iv, tc).cpu().numpy()
+        assert np.array_equal(got, pt), n
+        if n > 2:                                             # two shards, second uses C_{m-1} as its IV
+            m = n // 2
+            a = aes.cbc_decrypt(rk, iv, tc[:16 * m]).cpu().numpy()
+            b = aes.cbc_decrypt(rk, ct[16 * (m - 1):16 * m].tobytes(), tc[16 * m:]).cpu().numpy()
+            assert np.array_equal(np.r_[a, b], pt)
+    with pytest.raises(aes.AesError):
+        aes.cbc_decrypt(rk, iv, tc, out=tc)

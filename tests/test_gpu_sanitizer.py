@@ -1,0 +1,27 @@
+"""compute-sanitizer over the kernels: out-of-bounds tails,
+shared-memory races on the table fill, uninitialised reads, barrier misuse."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "initcheck", "synccheck"])
+def test_compute_sanitizer(tool):
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(cs):
+        pytest.skip("compute-sanitizer not found")
+    cmd = [cs, "--tool", tool, "--error-exitcode", "99"]
+    if tool == "memcheck":
+        cmd += ["--leak-check", "no"]
+    r = subprocess.run(cmd + [sys.executable, os.path.join(ROOT, "tools", "sanitize_smoke.py")],
+                       capture_output=True, text=True, timeout=1800, cwd=ROOT)
+    tail = (r.stdout + r.stderr)[-3000:]
+    assert r.returncode == 0, tail
+    assert "sanitize_smoke ok" in r.stdout, tail
+    assert "ERROR SUMMARY: 0 errors" in (r.stdout + r.stderr) or "RACECHECK SUMMARY: 0 hazards" in (r.stdout + r.stderr), tail

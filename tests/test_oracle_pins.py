@@ -292,3 +292,50 @@ def test_empty_and_bad_inputs():
         oracle.encrypt(bytes(15), bytes(16))
     with pytest.raises(ValueError):
         oracle.encrypt(bytes(16), bytes(17))
+
+
+# --------------------------------------------------------------------------
+# CTR (Eq 5, reading R24) and CBC (Eq 2, reading R25): SP 800-38A F.5 / F.2
+# --------------------------------------------------------------------------
+def _modes_golden():
+    rows = list(_lines("sp800_38a_ctr_cbc.txt"))
+    ctr_iv = bytes.fromhex(rows[0][1])
+    cbc_iv = bytes.fromhex(rows[1][1])
+    sets = []
+    for i in range(2, len(rows), 3):
+        sets.append((bytes.fromhex(rows[i][1]), bytes.fromhex("".join(rows[i + 1][1:])),
+                     bytes.fromhex("".join(rows[i + 2][1:]))))
+    pt = bytes.fromhex("".join(list(_lines("sp800_38a_ecb.txt"))[0][1:]))
+    return ctr_iv, cbc_iv, pt, sets
+
+
+def test_ctr_and_cbc_sp800_38a_vectors():
+    ctr_iv, cbc_iv, pt, sets = _modes_golden()
+    assert len(sets) == 3
+    for key, ctr_ct, cbc_ct in sets:
+        assert oracle.ctr(key, ctr_iv, pt).tobytes() == ctr_ct
+        assert oracle.ctr(key, ctr_iv, ctr_ct).tobytes() == pt          # CTR is an involution
+        assert oracle.cbc(key, cbc_iv, pt, False).tobytes() == cbc_ct
+        assert oracle.cbc(key, cbc_iv, cbc_ct, True).tobytes() == pt
+
+
+def test_ctr_counter_wrap_offset_and_openssl():
+    pytest.importorskip("cryptography")
+    from cryptography.hazmat.primitives.ciphers import Cipher, algorithms, modes
+    rng = np.random.default_rng(21)
+    for kb in (128, 256):
+        key = rng.integers(0, 256, kb // 8, dtype=np.uint8).tobytes()
+        for iv in (bytes([0xFF] * 16), bytes([0xFF] * 8) + bytes([0xFF] * 7) + b"\xfd",
+                   bytes(8) + bytes([0xFF] * 8), rng.integers(0, 256, 16, dtype=np.uint8).tobytes()):
+            data = rng.integers(0, 256, 16 * 37, dtype=np.uint8)
+            e = Cipher(algorithms.AES(key), modes.CTR(iv)).encryptor()
+            want = e.update(data.tobytes()) + e.finalize()
+            assert oracle.ctr(key, iv, data, nthreads=3).tobytes() == want
+            # block_offset k == the tail of a longer stream
+            assert oracle.ctr(key, iv, data[16 * 5:], block_offset=5).tobytes() == want[16 * 5:]
+        data = rng.integers(0, 256, 16 * 23, dtype=np.uint8)
+        iv = rng.integers(0, 256, 16, dtype=np.uint8).tobytes()
+        e = Cipher(algorithms.AES(key), modes.CBC(iv)).encryptor()
+        ct = e.update(data.tobytes()) + e.finalize()
+        assert oracle.cbc(key, iv, data, False).tobytes() == ct
+        assert oracle.cbc(key, iv, np.frombuffer(ct, np.uint8), True).tobytes() == data.tobytes()

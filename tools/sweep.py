@@ -68,7 +68,8 @@ def time_op(fn, s, reps, flush=None):
     ts = []
     for _ in range(reps):
         if flush is not None:
-            flush.zero_()
+            with torch.cuda.stream(s):
+                flush.zero_()          # on the timed stream, so it completes before e0
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(s):
             e0.record(s)
@@ -204,16 +205,55 @@ def ladder(a, s, hbm, ldsp):
                    paper_gpu_Bps=None)
 
 
+def modes(a, s, hbm, ldsp):
+    """NEXT-1 CTR and NEXT-4 CBC decryption at 1 GiB, all key sizes."""
+    nbytes = 1 << 30
+    x = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    synth.fill_device(x)
+    out = torch.empty_like(x)
+    n = nbytes // 16
+    iv = bytes(range(16))
+    for kb in (128, 192, 256):
+        key = synth.key(kb)
+        rk = aes.expand_key(key)
+        for mode in ("ctr", "cbc_dec"):
+            if mode == "ctr":
+                f = (lambda: aes.ctr_xcrypt(rk, iv, x, out=out))
+            else:
+                f = (lambda: aes.cbc_decrypt(rk, iv, x, out=out))
+            f()
+            torch.cuda.synchronize()
+            rng = np.random.default_rng(kb)
+            idx = np.unique(np.r_[0, 1, n - 1, rng.integers(0, n, 256)]).astype(np.int64)
+            got = out.view(-1, 16)[torch.from_numpy(idx).cuda()].cpu().numpy()
+            if mode == "ctr":
+                for i, g in zip(idx, got):
+                    w = oracle.ctr(key, iv, x.view(-1, 16)[int(i)].cpu().numpy().copy(), block_offset=int(i))
+                    assert np.array_equal(g, w), ("ctr parity", i)
+            else:
+                for i, g in zip(idx, got):
+                    prev = iv if i == 0 else x.view(-1, 16)[int(i) - 1].cpu().numpy().tobytes()
+                    w = oracle.cbc(key, prev, x.view(-1, 16)[int(i)].cpu().numpy().copy(), True)
+                    assert np.array_equal(g, w), ("cbc parity", i)
+            for _ in range(3):
+                f()
+            tmin, tmed = time_op(f, s, 10)
+            g = 8 * nbytes / tmin / 1e9
+            record(what="mode", mode=mode, keybits=kb, bytes=nbytes, t_min_s=tmin, t_med_s=tmed, Gbps=g,
+                   hbm_frac=(48 if mode == "cbc_dec" else 32) * n / tmin / 1e9 / hbm,
+                   lds_frac=16 * NR[kb] * n / tmin / ldsp)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--what", default="variants", choices=["sizes", "variants", "config3", "ladder", "all"])
+    ap.add_argument("--what", default="variants", choices=["sizes", "variants", "config3", "ladder", "modes", "all"])
     ap.add_argument("--big", action="store_true", help="include 16 GiB in the size sweep")
     a = ap.parse_args()
     s = torch.cuda.Stream()
     hbm = peaks()
     ldsp = lds_peak(s)
     record(what="peaks", hbm_gbs=hbm, lds_lookups_per_s=ldsp, gpu=torch.cuda.get_device_name(0))
-    todo = ["variants", "config3", "sizes", "ladder"] if a.what == "all" else [a.what]
+    todo = ["variants", "config3", "modes", "sizes", "ladder"] if a.what == "all" else [a.what]
     for w in todo:
         globals()[w](a, s, hbm, ldsp)
 
