@@ -124,7 +124,10 @@ def run_reference(a):
 # clocks during the timed region
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi sampled every 10 ms in the background; stop() keeps the
+    samples whose timestamps fall inside the timed window (all samples if the
+    window is shorter than the sampling period)."""
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -132,43 +135,57 @@ class ClockSampler:
         self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
         self.gpu = gpu_index
         self.p = None
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
             self.f = open(self.path, "w")
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "10"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
     def stop(self):
         if not self.p:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)
         self.p.terminate()
         try:
             self.p.wait(timeout=5)
         except Exception:
             self.p.kill()
         self.f.close()
-        sm, smax, reasons, power = [], [], set(), []
+        import datetime
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         for ln in open(self.path):
             f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
             try:
-                sm.append(float(f[1])); smax.append(float(f[2])); power.append(float(f[3]))
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(f[2]), float(f[3]), float(f[4]),
+                             [n for n, v in zip(names, f[6:10]) if v.lower().startswith("active")]))
             except ValueError:
                 continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
         os.unlink(self.path)
-        if not sm:
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
-                "samples": len(sm), "power_w_max": max(power)}
+        inside = [r for r in rows if self.t0 is not None and self.t0 - 0.01 <= r[0] <= self.t1 + 0.01]
+        window = "timed region" if inside else "around the timed region (window shorter than sampling)"
+        if not inside:
+            mid = (self.t0 + self.t1) / 2 if self.t0 else rows[len(rows) // 2][0]
+            inside = sorted(rows, key=lambda r: abs(r[0] - mid))[:3]
+        return {"sm_mhz": statistics.median(r[1] for r in inside), "sm_max_mhz": max(r[2] for r in inside),
+                "reasons": sorted({x for r in inside for x in r[4]}), "samples": len(inside),
+                "power_w_max": max(r[3] for r in inside), "window": window}
 
 
 def measured_peaks():
@@ -199,11 +216,14 @@ def run_ours(a):
     import torch
 
     from paper_1902_05234_b200 import dist as pdist
-    rank, world, local = pdist.init()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # AES_BENCH_BACKEND=gloo lets the N>1 code path run with several ranks on
+    # one GPU (harness validation only; the driver's N>1 runs use NCCL, one GPU each)
+    backend = os.environ.get("AES_BENCH_BACKEND") or None
+    rank, world, local = pdist.init(backend)
+    dev = torch.device("cuda", local % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
 
     import paper_1902_05234_b200 as aes   # ImportError if libaes_b200.so is missing
     import synth
@@ -271,17 +291,19 @@ def run_ours(a):
     K = a.steps
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clk = ClockSampler(local)
+    clk = ClockSampler(dev.index)
     clk.start()
     time.sleep(0.3)
     pdist.barrier(dev)
     torch.cuda.synchronize(dev)
+    clk.mark_start()
     with torch.cuda.stream(s):
         t_start.record(s)
         for k in range(K):
             step(evs[k])
         t_end.record(s)
     s.synchronize()
+    clk.mark_end()
     torch.cuda.synchronize(dev)
     pdist.barrier(dev)
     clocks = clk.stop()

@@ -76,6 +76,23 @@ def expand_key(key: bytes) -> RoundKeys:
     return RoundKeys(rk)
 
 
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+_NULL = _Null()
+
+
+def _on_device(dev):
+    """torch.cuda.device(dev) only when dev is not already current (cheap path)."""
+    import torch
+    return _NULL if dev.index == torch.cuda.current_device() else torch.cuda.device(dev)
+
+
 def _check_tensor(x, name):
     import torch
     if not isinstance(x, torch.Tensor):
@@ -101,9 +118,9 @@ def ecb(rk: RoundKeys, x, decrypt: bool, out=None, variant: int = AES_VAR_DEFAUL
         _check_tensor(out, "out")
         if out.numel() != x.numel():
             raise ValueError("out must have the same size as x")
-    s = stream if stream is not None else torch.cuda.current_stream(x.device)
     n = x.numel() // 16
-    with torch.cuda.device(x.device):
+    with _on_device(x.device):
+        s = stream if stream is not None else torch.cuda.current_stream()
         if variant == AES_VAR_DEFAULT and not states_per_thread and not grid:
             fn = _native.lib.aes_ecb_decrypt if decrypt else _native.lib.aes_ecb_encrypt
             code = fn(ctypes.byref(rk.c), rk.nr, ctypes.c_void_p(x.data_ptr()),
@@ -143,8 +160,8 @@ def ctr_xcrypt(rk: RoundKeys, iv: bytes, x, out=None, block_offset: int = 0, str
     if len(iv) != 16:
         raise ValueError("iv must be 16 bytes")
     out = _prep_out(x, out)
-    s = stream if stream is not None else torch.cuda.current_stream(x.device)
-    with torch.cuda.device(x.device):
+    with _on_device(x.device):
+        s = stream if stream is not None else torch.cuda.current_stream()
         code = _native.lib.aes_ctr_xcrypt(ctypes.byref(rk.c), rk.nr, iv, block_offset & (2**64 - 1),
                                           ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                           x.numel() // 16, ctypes.c_void_p(s.cuda_stream))
@@ -159,8 +176,8 @@ def cbc_decrypt(rk: RoundKeys, iv: bytes, x, out=None, stream=None):
     if len(iv) != 16:
         raise ValueError("iv must be 16 bytes")
     out = _prep_out(x, out)
-    s = stream if stream is not None else torch.cuda.current_stream(x.device)
-    with torch.cuda.device(x.device):
+    with _on_device(x.device):
+        s = stream if stream is not None else torch.cuda.current_stream()
         code = _native.lib.aes_cbc_decrypt(ctypes.byref(rk.c), rk.nr, iv, ctypes.c_void_p(x.data_ptr()),
                                            ctypes.c_void_p(out.data_ptr()), x.numel() // 16,
                                            ctypes.c_void_p(s.cuda_stream))

@@ -101,17 +101,25 @@ struct Tab<V_REPL> {
         const uint32_t* src = DEC ? &g_tab.td[0][0] : &g_tab.te[0][0];
         uint4* s4 = reinterpret_cast<uint4*>(smem);
         // regions A,B: 32768 words; word w -> x = (w>>6)&255, table i = 2*(w>>14) + ((w>>5)&1)
-        for (int q = threadIdx.x; q < 8192; q += blockDim.x) {
-            int w = 4 * q;
+        // blockDim.x == kThreads: fixed trip counts, fully unrolled so every
+        // (L2-resident) table load of a thread is in flight at once
+        uint32_t v[8192 / kThreads];
+#pragma unroll
+        for (int it = 0; it < 8192 / kThreads; it++) {
+            int w = 4 * (threadIdx.x + it * kThreads);
             int x = (w >> 6) & 255, i = 2 * (w >> 14) + ((w >> 5) & 1);
-            uint32_t v = src[i * 256 + x];
-            s4[q] = make_uint4(v, v, v, v);
+            v[it] = __ldg(src + i * 256 + x);
         }
+#pragma unroll
+        for (int it = 0; it < 8192 / kThreads; it++)
+            s4[threadIdx.x + it * kThreads] = make_uint4(v[it], v[it], v[it], v[it]);
         if (DEC) {
-            for (int q = threadIdx.x; q < 256 * 8; q += blockDim.x) {
+#pragma unroll
+            for (int it = 0; it < 2048 / kThreads; it++) {
+                int q = threadIdx.x + it * kThreads;
                 int x = q >> 3, part = q & 7;
-                uint32_t v = g_tab.si4[x];
-                s4[(kOffSi + x * 256) / 16 + part] = make_uint4(v, v, v, v);
+                uint32_t u = __ldg(g_tab.si4 + x);
+                s4[(kOffSi + x * 256) / 16 + part] = make_uint4(u, u, u, u);
             }
         }
         __syncthreads();
@@ -473,7 +481,10 @@ aes_status launch(const aes_round_keys* rk, int nr, int decrypt, const void* in,
     }
     int occ = 1, nsm = 148;
     if ((st = resident_ctas(dev, ki, &occ, &nsm))) return st;
-    uint64_t per_cta = (uint64_t)kThreads * spt;
+    // Spread small and medium buffers over every SM (at least one full warp of
+    // states per CTA) instead of packing 1024 states into each CTA: the per-CTA
+    // table fill is ~0.5 us, the lookups are what must be parallel.
+    uint64_t per_cta = 32ull * spt;
     uint64_t want = (nblocks + per_cta - 1) / per_cta;
     uint64_t cap = grid_req ? (uint64_t)grid_req : (uint64_t)nsm * occ;
     unsigned grid = (unsigned)(want < cap ? want : cap);

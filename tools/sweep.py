@@ -80,6 +80,18 @@ def time_op(fn, s, reps, flush=None):
     return min(ts), statistics.median(ts)
 
 
+def time_b2b(fn, s, reps):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        fn()
+        e0.record(s)
+        for _ in range(reps):
+            fn()
+        e1.record(s)
+    s.synchronize()
+    return e0.elapsed_time(e1) * 1e-3 / reps
+
+
 def record(**kw):
     print(json.dumps(kw), flush=True)
 
@@ -109,11 +121,15 @@ def sizes(a, s, hbm, ldsp):
                 for _ in range(3):
                     f()
                 tmin, tmed = time_op(f, s, reps, None if warm else flush)
+                tb2b = time_b2b(f, s, 20 if nbytes < (256 << 20) else 3)
                 g = 8 * nbytes / tmin / 1e9
                 fits.setdefault((kb, dec), []).append((n, tmin))
                 record(what="size", bytes=nbytes, keybits=kb, dir="dec" if dec else "enc", t_min_s=tmin,
                        t_med_s=tmed, Gbps=g, GBps=g / 8, hbm_frac=32 * n / tmin / 1e9 / hbm,
-                       lds_frac=16 * NR[kb] * n / tmin / ldsp, l2="flushed" if not warm else "input>2xL2")
+                       lds_frac=16 * NR[kb] * n / tmin / ldsp, l2="flushed" if not warm else "input>2xL2",
+                       t_b2b_s=tb2b, Gbps_b2b=8 * nbytes / tb2b / 1e9,
+                       note="t_min: one call incl. host launch path (L2 flushed if small); "
+                            "t_b2b: mean of back-to-back launches (device time, L2 warm if small)")
         del x, out
         torch.cuda.empty_cache()
     for (kb, dec), pts in fits.items():
