@@ -196,13 +196,16 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)", {}
 
 
-def ncu_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+def ncu_traffic(alg_bytes):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/ncu_summary.json), if it was taken at this launch size."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(p):
         try:
             d = json.load(open(p))
-            return d.get("dominant_kernel_dram_bytes_per_launch"), d.get("source")
+            if d.get("algorithmic_bytes_per_launch") == alg_bytes:
+                return d.get("dominant_kernel_dram_bytes_per_launch"), d.get("source")
+            return None, "no ncu capture at this launch size"
         except Exception:
             pass
     return None, None
@@ -347,7 +350,7 @@ def run_ours(a):
     kern_ms = max(enc_ms, dec_ms)
     dom = "encrypt" if enc_ms >= dec_ms else "decrypt"
     achieved = 32.0 * n / (kern_ms * 1e-3) / 1e9               # GB/s, 16 B read + 16 B written per block
-    traffic, traffic_src = ncu_traffic()
+    traffic, traffic_src = ncu_traffic(32 * n)
     lookups = 16 * NR * n
     sm_clk = clocks.get("sm_mhz") or 1965.0
     lds_nominal = nsm * 32 * sm_clk * 1e6
@@ -373,9 +376,10 @@ def run_ours(a):
             "metric": METRIC, "value": gbps, "unit": "Gbps", "n_gpus": world, "steps": K, "warmup": a.warmup,
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u8", "data": "synthetic (splitmix64 counter stream, seed 190205234; random-init key)",
-            "config": {"workload": WORKLOAD, "keybits": KEYBITS, "bytes_per_gpu": nbytes,
+            "config": {"workload": WORKLOAD if nbytes == GIB else WORKLOAD.replace("1 GiB", f"{nbytes / GIB:g} GiB"),
+                       "keybits": KEYBITS, "bytes_per_gpu": nbytes,
                        "global_bytes": nbytes * world, "parallelism": f"dp{world} (contiguous block shards)",
-                       "step": "expand_key + encrypt(1 GiB) + decrypt(1 GiB)",
+                       "step": f"expand_key + encrypt({nbytes / GIB:g} GiB) + decrypt({nbytes / GIB:g} GiB)",
                        "l2": "inputs (1 GiB) larger than L2 (126 MB); no flush",
                        "variant": "smem_repl, 1 state/thread, persistent grid"},
             "GBps": gbps / 8, "enc_ms": enc_ms, "dec_ms": dec_ms,

@@ -273,3 +273,31 @@ def test_cbc_decrypt_against_oracle_and_sharding(aes, keybits):
             assert np.array_equal(np.r_[a, b], pt)
     with pytest.raises(aes.AesError):
         aes.cbc_decrypt(rk, iv, tc, out=tc)
+
+
+def test_config5_64gib_in_place_block_indices_past_2_32(aes):
+    """BASELINE config 5's buffer on one GPU: 64 GiB = 2^32 blocks (block
+    indices and byte offsets beyond 32 bits), AES-128 encrypt in place,
+    sampled oracle parity around block 2^32-1 and at both ends, then decrypt
+    in place and check the same samples against the generator."""
+    free, _ = torch.cuda.mem_get_info()
+    nbytes = 64 << 30
+    if free < nbytes + (4 << 30):
+        pytest.skip("needs ~68 GiB free")
+    n = nbytes // 16
+    key = synth.key(128)
+    rk = aes.expand_key(key)
+    x = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    synth.fill_device(x)
+    aes.ecb_encrypt(rk, x, out=x)
+    idx = _sample_idx(n, k=2048, seed=5)
+    idx = np.unique(np.r_[idx, n - 1, n - 2, (1 << 32) - 1, (1 << 28), (1 << 28) - 1])
+    idx = idx[idx < n]
+    plain = synth.blocks_at(idx.astype(np.uint64)).reshape(-1)
+    tidx = torch.from_numpy(idx).cuda()
+    got = x.view(-1, 16)[tidx].cpu().numpy().reshape(-1)
+    assert np.array_equal(got, oracle.encrypt(key, plain, nthreads=8))
+    aes.ecb_decrypt(rk, x, out=x)
+    assert np.array_equal(x.view(-1, 16)[tidx].cpu().numpy().reshape(-1), plain)
+    del x
+    torch.cuda.empty_cache()

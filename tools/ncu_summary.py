@@ -84,6 +84,9 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--tag", required=True)
     ap.add_argument("--note", default="")
+    ap.add_argument("--alg-bytes", type=float, default=None,
+                    help="algorithmic HBM bytes per launch of the captured kernels (32 B x blocks)")
+    ap.add_argument("--primary", action="store_true", help="also write profiles/ncu_summary.json (read by bench.py)")
     a = ap.parse_args()
     prof = os.path.join(ROOT, "profiles")
     os.makedirs(prof, exist_ok=True)
@@ -98,6 +101,7 @@ def main():
         summary["dominant_kernel"] = dom["kernel"]
         summary["dominant_kernel_dram_bytes_per_launch"] = dom["dram_bytes"]
         summary["source"] = f"ncu --set full, {os.path.basename(a.rep)} ({a.tag})"
+        summary["algorithmic_bytes_per_launch"] = a.alg_bytes
         md += ["## `ncu --set full` (one launch each)", "", "| metric | " + " | ".join(k["kernel"][:48] for k in ks) + " |",
                "|---|" + "---|" * len(ks)]
         for key, name in KEYS:
@@ -119,7 +123,8 @@ def main():
         summary["launches"] = {k: {"count": c, "total_ns": t} for k, (c, t) in agg.items()}
         shutil.copy(a.launches, os.path.join(prof, f"{a.tag}_launches.csv"))
     json.dump(summary, open(os.path.join(prof, f"{a.tag}_ncu_summary.json"), "w"), indent=1)
-    json.dump(summary, open(os.path.join(prof, "ncu_summary.json"), "w"), indent=1)
+    if a.primary:
+        json.dump(summary, open(os.path.join(prof, "ncu_summary.json"), "w"), indent=1)
     open(os.path.join(prof, f"{a.tag}_ncu_summary.md"), "w").write("\n".join(md))
     print("\n".join(md))
 
