@@ -340,10 +340,25 @@ def run_ours(a):
         dt = pdist.max_over_ranks(time.perf_counter() - t0, dev)
         pipe.close()
         assert torch.equal(hp, hx)
+        # the path's own roofline: the host link with H2D and D2H running at once
+        s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        tl = []
+        for _ in range(3):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            with torch.cuda.stream(s1):
+                pt.copy_(hx, non_blocking=True)
+            with torch.cuda.stream(s2):
+                hp.copy_(ct, non_blocking=True)
+            torch.cuda.synchronize(dev)
+            tl.append(time.perf_counter() - t0)
+        link = nbytes / min(tl) / 1e9
         e2e = {"value": 8 * pdist.sum_over_ranks(2.0 * nbytes * KE, dev) / dt / 1e9, "unit": "Gbps",
                "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": 2 * nbytes,
                "steps": KE, "timing": "host perf_counter around synchronous aes_pipeline_run calls, max over ranks",
-               "path": "aes_pipeline_run: pinned host -> H2D -> kernel -> D2H, 64 MiB chunks x 4 streams"}
+               "path": "aes_pipeline_run: pinned host -> H2D -> kernel -> D2H, 64 MiB chunks x 4 streams",
+               "link_GBps_each_direction": link,
+               "link_frac": (2.0 * nbytes * KE / dt / 1e9 / 2) / link}
 
     # ---- roofline of the dominant kernel ---------------------------------
     peak, peak_src, peaks = measured_peaks()

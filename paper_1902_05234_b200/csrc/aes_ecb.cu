@@ -550,15 +550,14 @@ aes_status aes_cbc_decrypt(const aes_round_keys* rk, int nr, const uint8_t* iv, 
 aes_status aes_mb_lds_gather(void* sink, int grid, int iters, void* stream) {
     if (!sink) return AES_ENULL;
     if (grid <= 0 || iters < 0) return AES_ERANGE;
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(reinterpret_cast<const void*>(&lds_gather_kernel),
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemReplEnc);
-    });
-    if (attr_err != cudaSuccess) return cuda_fail(attr_err);
+    int dev = 0, occ = 1, nsm = 148;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    KernelInfo ki{reinterpret_cast<const void*>(&lds_gather_kernel), kSmemReplEnc};
+    aes_status st = resident_ctas(dev, ki, &occ, &nsm);   // sets the smem attribute once per device
+    if (st) return st;
     lds_gather_kernel<<<grid, kThreads, kSmemReplEnc, (cudaStream_t)stream>>>(static_cast<uint32_t*>(sink), iters);
-    cudaError_t e = cudaGetLastError();
+    e = cudaGetLastError();
     return e == cudaSuccess ? AES_OK : cuda_fail(e);
 }
 

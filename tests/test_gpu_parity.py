@@ -301,3 +301,37 @@ def test_config5_64gib_in_place_block_indices_past_2_32(aes):
     assert np.array_equal(x.view(-1, 16)[tidx].cpu().numpy().reshape(-1), plain)
     del x
     torch.cuda.empty_cache()
+
+
+def test_host_threads_call_concurrently(aes):
+    """The ABI is re-entrant: 8 host threads, each with its own key and stream."""
+    import threading
+    n = 4099
+    host = synth.blocks(0, n)
+    x = _dev_rand(n)
+    results, errors = {}, []
+
+    def work(t):
+        try:
+            kb = (128, 192, 256)[t % 3]
+            key = bytes((t * 31 + i) & 0xFF for i in range(kb // 8))
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(20):
+                    rk = aes.expand_key(key)
+                    ct = aes.ecb_encrypt(rk, x)
+                    back = aes.ecb_decrypt(rk, ct)
+            s.synchronize()
+            results[t] = (key, ct.cpu().numpy(), bool(torch.equal(back, x)))
+        except Exception as e:   # pragma: no cover
+            errors.append(e)
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(8)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors
+    for t, (key, ct, ok) in results.items():
+        assert ok
+        assert np.array_equal(ct, oracle.encrypt(key, host, nthreads=4)), t
