@@ -358,7 +358,7 @@ def run_ours(a):
                "steps": KE, "timing": "host perf_counter around synchronous aes_pipeline_run calls, max over ranks",
                "path": "aes_pipeline_run: pinned host -> H2D -> kernel -> D2H, 64 MiB chunks x 4 streams",
                "link_GBps_each_direction": link,
-               "link_frac": (2.0 * nbytes * KE / dt / 1e9 / 2) / link}
+               "link_frac": (2.0 * nbytes * KE / dt / 1e9) / link}   # bytes each way per second / ceiling
 
     # ---- roofline of the dominant kernel ---------------------------------
     peak, peak_src, peaks = measured_peaks()
