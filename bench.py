@@ -42,7 +42,8 @@ def parse():
     ap.add_argument("--bytes-per-gpu", type=int, default=GIB)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample length for cpu_baseline")
+    ap.add_argument("--ref-seconds", type=float, default=0.0, help="oracle seconds per --impl reference step (0 = auto)")
     return ap.parse_args()
 
 
@@ -95,7 +96,7 @@ def run_reference(a):
     if rank != 0:
         return 0
     cores = host_cores()
-    per_step = max(1.0, min(20.0, 150.0 / max(1, a.steps + a.warmup)))
+    per_step = a.ref_seconds if a.ref_seconds else max(1.0, min(20.0, 150.0 / max(1, a.steps + a.warmup)))
     for _ in range(a.warmup):
         time_oracle(per_step / 4, cores)
     vals, secs = [], 0.0

@@ -154,6 +154,8 @@ aes_status aes_ecb_launch(const aes_round_keys *rk, int nr, int decrypt, const v
  * complete (synchronous).  in_host/out_host: host memory, 16*nblocks bytes,
  * ideally page-locked (pageable memory works but does not overlap);
  * in_host == out_host allowed.  chunk_bytes: multiple of 16, >= 16; depth 1..8.
+ * A pipeline object is not re-entrant (its staging buffers are shared): use
+ * one per host thread.  Pipelines on different devices are independent.
  * Errors: AES_ENULL, AES_ERANGE, AES_ENR, AES_EOVERLAP, AES_ECUDA. */
 typedef struct aes_pipeline aes_pipeline;
 aes_status aes_pipeline_create(uint64_t chunk_bytes, int depth, aes_pipeline **out);

@@ -1,0 +1,56 @@
+"""bench.py contract: the JSON line's keys, on CPU (--impl reference) and on
+the GPU (our arm at N=1, and the N=2 code path with two gloo ranks sharing
+one GPU)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+        "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"}
+
+
+def _last_json(out):
+    lines = [ln for ln in out.splitlines() if ln.startswith("{")]
+    assert lines, out[-2000:]
+    return json.loads(lines[-1])
+
+
+def test_reference_arm_on_cpu():
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0",
+                        "--ref-seconds", "1"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = _last_json(r.stdout)
+    assert KEYS <= set(d)
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "Gbps"
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+@pytest.mark.gpu
+def test_bench_our_arm_n1():
+    r = subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--bytes-per-gpu",
+                        str(64 << 20), "--cpu-seconds", "1"], cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _last_json(r.stdout)
+    assert KEYS <= set(d) and {"roofline", "roofline_lds", "clocks", "gpu_launches"} <= set(d)
+    assert d["n_gpus"] == 1 and d["value"] > 100 and d["gpu_launches"] == 6
+    assert d["roofline"]["bound"] == "hbm" and 0 < d["roofline"]["frac"] < 1.2
+    assert d["e2e"]["h2d_bytes_per_step"] == 2 * (64 << 20)
+    assert d["cpu_baseline"]["kind"] == "oracle"
+
+
+@pytest.mark.gpu
+def test_bench_n2_code_path_with_gloo_on_one_gpu():
+    env = dict(os.environ, AES_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2",
+                        "--steps", "3", "--warmup", "3", "--bytes-per-gpu", str(32 << 20)],
+                       cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _last_json(r.stdout)
+    assert d["n_gpus"] == 2 and d["config"]["global_bytes"] == 2 * (32 << 20)
+    assert d["cpu_baseline"] is None and d["gpu_launches"] == 6
