@@ -87,6 +87,15 @@ class _Null:
 _NULL = _Null()
 
 
+def _raw_stream(dev_index: int) -> int:
+    """cudaStream_t of torch's current stream on ``dev_index`` (cheap path)."""
+    import torch
+    try:
+        return torch._C._cuda_getCurrentRawStream(dev_index)
+    except AttributeError:   # pragma: no cover - older torch
+        return torch.cuda.current_stream(dev_index).cuda_stream
+
+
 def _on_device(dev):
     """torch.cuda.device(dev) only when dev is not already current (cheap path)."""
     import torch
@@ -120,16 +129,14 @@ def ecb(rk: RoundKeys, x, decrypt: bool, out=None, variant: int = AES_VAR_DEFAUL
             raise ValueError("out must have the same size as x")
     n = x.numel() // 16
     with _on_device(x.device):
-        s = stream if stream is not None else torch.cuda.current_stream()
+        sp = stream.cuda_stream if stream is not None else _raw_stream(x.device.index)
         if variant == AES_VAR_DEFAULT and not states_per_thread and not grid:
             fn = _native.lib.aes_ecb_decrypt if decrypt else _native.lib.aes_ecb_encrypt
-            code = fn(ctypes.byref(rk.c), rk.nr, ctypes.c_void_p(x.data_ptr()),
-                      ctypes.c_void_p(out.data_ptr()), n, ctypes.c_void_p(s.cuda_stream))
+            code = fn(ctypes.byref(rk.c), rk.nr, x.data_ptr(), out.data_ptr(), n, sp)
         else:
             cfg = aes_launch_config(variant, states_per_thread, grid, 0)
             code = _native.lib.aes_ecb_launch(ctypes.byref(rk.c), rk.nr, int(bool(decrypt)),
-                                              ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()),
-                                              n, ctypes.c_void_p(s.cuda_stream), ctypes.byref(cfg))
+                                              x.data_ptr(), out.data_ptr(), n, sp, ctypes.byref(cfg))
     _check(code, "aes_ecb_decrypt" if decrypt else "aes_ecb_encrypt")
     return out
 
@@ -161,10 +168,9 @@ def ctr_xcrypt(rk: RoundKeys, iv: bytes, x, out=None, block_offset: int = 0, str
         raise ValueError("iv must be 16 bytes")
     out = _prep_out(x, out)
     with _on_device(x.device):
-        s = stream if stream is not None else torch.cuda.current_stream()
+        sp = stream.cuda_stream if stream is not None else _raw_stream(x.device.index)
         code = _native.lib.aes_ctr_xcrypt(ctypes.byref(rk.c), rk.nr, iv, block_offset & (2**64 - 1),
-                                          ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()),
-                                          x.numel() // 16, ctypes.c_void_p(s.cuda_stream))
+                                          x.data_ptr(), out.data_ptr(), x.numel() // 16, sp)
     _check(code, "aes_ctr_xcrypt")
     return out
 
@@ -177,10 +183,9 @@ def cbc_decrypt(rk: RoundKeys, iv: bytes, x, out=None, stream=None):
         raise ValueError("iv must be 16 bytes")
     out = _prep_out(x, out)
     with _on_device(x.device):
-        s = stream if stream is not None else torch.cuda.current_stream()
-        code = _native.lib.aes_cbc_decrypt(ctypes.byref(rk.c), rk.nr, iv, ctypes.c_void_p(x.data_ptr()),
-                                           ctypes.c_void_p(out.data_ptr()), x.numel() // 16,
-                                           ctypes.c_void_p(s.cuda_stream))
+        sp = stream.cuda_stream if stream is not None else _raw_stream(x.device.index)
+        code = _native.lib.aes_cbc_decrypt(ctypes.byref(rk.c), rk.nr, iv, x.data_ptr(), out.data_ptr(),
+                                           x.numel() // 16, sp)
     _check(code, "aes_cbc_decrypt")
     return out
 

@@ -58,6 +58,14 @@ def read_rep(rep):
         rb = to_bytes(d["dram__bytes_read.sum"], units[hdr.index("dram__bytes_read.sum")])
         wb = to_bytes(d["dram__bytes_write.sum"], units[hdr.index("dram__bytes_write.sum")])
         k["dram_bytes"] = rb + wb
+        stalls = []
+        for key, v in d.items():
+            if key.startswith("smsp__average_warps_issue_stalled_") and key.endswith("_per_issue_active.ratio"):
+                try:
+                    stalls.append((key[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")], float(v)))
+                except ValueError:
+                    pass
+        k["stalls_per_issue"] = dict(sorted(stalls, key=lambda x: -x[1])[:6])
         lds_i = float(d.get("smsp__sass_inst_executed_op_shared_ld.sum", "0") or 0)
         lds_w = float(d.get("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "0") or 0)
         k["wavefronts_per_lds"] = lds_w / lds_i if lds_i else None
@@ -110,6 +118,8 @@ def main():
         md.append("| DRAM bytes (read+write) | " + " | ".join(f'{k["dram_bytes"]:.4g}' for k in ks) + " |")
         md.append("| LDS wavefronts per LDS instruction | " + " | ".join(
             f'{k["wavefronts_per_lds"]:.4f}' if k["wavefronts_per_lds"] else "-" for k in ks) + " |")
+        md.append("| top warp stall reasons (warps per issue) | " + " | ".join(
+            ", ".join(f"{n} {v:.2f}" for n, v in list(k["stalls_per_issue"].items())[:4]) for k in ks) + " |")
         md.append("")
         shutil.copy(a.rep, os.path.join(prof, f"{a.tag}_full.ncu-rep")) if os.path.getsize(a.rep) < 8 << 20 else None
     if a.launches:
