@@ -1,0 +1,99 @@
+#!/usr/bin/env python
+"""BASELINE config 5: AES-128 ECB encrypt of a 64 GiB buffer (2^32 blocks)
+sharded across N GPUs -- strong scaling (total work fixed).
+
+    python tools/scale.py                                   # N = 1 (64 GiB on one GPU, in place)
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/scale.py
+
+Rank r owns blocks [r*n/N, (r+1)*n/N) of the global splitmix64 stream
+(dist.shard_range), fills them on its own GPU, checks sampled blocks against
+the oracle (including the shard edges and block 2^32-1), and then encrypts its
+shard in place K times.  Time = max over ranks of the CUDA-event time of the K
+launches between two barriers.  No data-path collective.  One JSON line.
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+import torch
+
+import oracle
+import paper_1902_05234_b200 as aes
+import synth
+from paper_1902_05234_b200 import dist as pdist
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--global-bytes", type=int, default=64 << 30)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    a = ap.parse_args()
+    rank, world, local = pdist.init(os.environ.get("AES_BENCH_BACKEND") or None)
+    dev = torch.device("cuda", local % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    n = a.global_bytes // 16
+    b0, b1 = pdist.shard_range(n, rank, world)
+    m = b1 - b0
+    key = synth.key(128)
+    rk = aes.expand_key(key)
+    x = torch.empty(16 * m, dtype=torch.uint8, device=dev)
+    s = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(s):
+        synth.fill_device(x, first_block=b0)
+        aes.ecb_encrypt(rk, x, out=x)
+    s.synchronize()
+    rng = np.random.default_rng(rank)
+    loc = np.unique(np.r_[0, 1, m - 2, m - 1, rng.integers(0, m, 1024)])
+    g = b0 + loc
+    if b0 <= (1 << 32) - 1 < b1:
+        loc = np.unique(np.r_[loc, (1 << 32) - 1 - b0])
+        g = b0 + loc
+    loc = loc[loc < m]
+    g = b0 + loc
+    tidx = torch.from_numpy(loc.astype(np.int64)).to(dev)
+    want = oracle.encrypt(key, synth.blocks_at(g.astype(np.uint64)).reshape(-1), nthreads=8)
+    ok = np.array_equal(x.view(-1, 16)[tidx].cpu().numpy().reshape(-1), want)
+    with torch.cuda.stream(s):
+        aes.ecb_decrypt(rk, x, out=x)
+    s.synchronize()
+    ok &= np.array_equal(x.view(-1, 16)[tidx].cpu().numpy().reshape(-1), synth.blocks_at(g.astype(np.uint64)).reshape(-1))
+    if pdist.sum_over_ranks(0.0 if ok else 1.0, dev):
+        if rank == 0:
+            print(json.dumps({"error": "parity failed"}))
+        return 1
+    with torch.cuda.stream(s):
+        for _ in range(a.warmup):
+            aes.ecb_encrypt(rk, x, out=x)
+    s.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pdist.barrier(dev)
+    torch.cuda.synchronize(dev)
+    with torch.cuda.stream(s):
+        e0.record(s)
+        for _ in range(a.steps):
+            aes.ecb_encrypt(rk, x, out=x)
+        e1.record(s)
+    s.synchronize()
+    pdist.barrier(dev)
+    ms = pdist.max_over_ranks(e0.elapsed_time(e1), dev)
+    total = pdist.sum_over_ranks(16.0 * m * a.steps, dev)
+    if rank == 0:
+        gbps = 8 * total / (ms * 1e-3) / 1e9
+        print(json.dumps({"metric": "AES-128 ECB encrypt Gbps, 64 GiB sharded (BASELINE config 5)",
+                          "value": gbps, "unit": "Gbps", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+                          "ms_per_step": ms / a.steps, "scaling": "strong", "global_bytes": a.global_bytes,
+                          "bytes_per_gpu": 16 * m, "GBps": gbps / 8,
+                          "hbm_frac": 32 * total / 16 / (ms * 1e-3) / 1e9 / 6550.7 / world,
+                          "parity": "sampled blocks incl. shard edges and block 2^32-1 vs oracle; in-place round trip",
+                          "gpu": torch.cuda.get_device_name(dev)}), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
