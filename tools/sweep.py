@@ -120,6 +120,7 @@ def sizes(a, s, hbm, ldsp):
                 warm = nbytes >= 2 * l2
                 for _ in range(3):
                     f()
+                torch.cuda.synchronize()   # warm-ups ran on the default stream; s is non-blocking
                 tmin, tmed = time_op(f, s, reps, None if warm else flush)
                 tb2b = time_b2b(f, s, 20 if nbytes < (256 << 20) else 3)
                 g = 8 * nbytes / tmin / 1e9
@@ -182,6 +183,7 @@ def config3(a, s, hbm, ldsp):
     parity(key, ct, out, True)
     for _ in range(3):
         f()
+    torch.cuda.synchronize()   # warm-ups ran on the default stream; s is non-blocking
     tmin, tmed = time_op(f, s, 10)
     n = nbytes // 16
     g = 8 * nbytes / tmin / 1e9
@@ -253,6 +255,7 @@ def modes(a, s, hbm, ldsp):
                     assert np.array_equal(g, w), ("cbc parity", i)
             for _ in range(3):
                 f()
+            torch.cuda.synchronize()   # warm-ups ran on the default stream; s is non-blocking
             tmin, tmed = time_op(f, s, 10)
             g = 8 * nbytes / tmin / 1e9
             record(what="mode", mode=mode, keybits=kb, bytes=nbytes, t_min_s=tmin, t_med_s=tmed, Gbps=g,
