@@ -163,6 +163,16 @@ aes_status aes_pipeline_run(aes_pipeline *p, const aes_round_keys *rk, int nr, i
                             const void *in_host, void *out_host, uint64_t nblocks);
 aes_status aes_pipeline_destroy(aes_pipeline *p);
 
+/* aes_ecb_trace: parity pin for single rounds (SURVEY.md 8(c) "per-round
+ * states"; FIPS-197 App B).  Writes, for each block, the state after
+ * AddRoundKey(0) and `rounds` Eq 26 rounds (0 <= rounds <= nr; rounds == nr
+ * is the full cipher incl. the final round) computed by the same round code
+ * the production kernels use.  decrypt = 1 runs the equivalent inverse cipher
+ * with dk.  Same buffer contract as aes_ecb_encrypt; AES_ERANGE for a bad
+ * `rounds`.  Test/debug use; not tuned. */
+aes_status aes_ecb_trace(const aes_round_keys *rk, int nr, int decrypt, int rounds, const void *in, void *out,
+                         uint64_t nblocks, void *stream);
+
 /* Shared-memory gather microbenchmark (the binding roofline):
  * `grid` CTAs x 1024 threads each perform `iters` x 16 conflict-free 32-bit
  * lookups into a lane-replicated 128 KiB table with the same one-PRMT address

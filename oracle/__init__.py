@@ -54,6 +54,7 @@ def lib():
             L.oracle_aes_ecb.restype = i32
             L.oracle_aes_ecb.argtypes = [p, i32, i32, p, p, u64, i32]
             L.oracle_cipher_trace.restype = i32; L.oracle_cipher_trace.argtypes = [p, i32, p, p]
+            L.oracle_inv_cipher_trace.restype = i32; L.oracle_inv_cipher_trace.argtypes = [p, i32, p, p]
             L.oracle_sbox_table.restype = None; L.oracle_sbox_table.argtypes = [p]
             L.oracle_inv_sbox_table.restype = None; L.oracle_inv_sbox_table.argtypes = [p]
             L.oracle_transform.restype = i32; L.oracle_transform.argtypes = [i32, p]
@@ -118,6 +119,14 @@ def cipher_trace(key: bytes, block: bytes) -> list[bytes]:
     n = nr(8 * len(key))
     tr = ctypes.create_string_buffer(16 * (n + 1))
     lib().oracle_cipher_trace(_buf(key), 8 * len(key), _buf(block), tr)
+    return [tr.raw[16 * r:16 * r + 16] for r in range(n + 1)]
+
+
+def inv_cipher_trace(key: bytes, block: bytes) -> list[bytes]:
+    """InvCipher states: [after ARK(Nr), after iteration Nr-1, ..., after iteration 1, output]."""
+    n = nr(8 * len(key))
+    tr = ctypes.create_string_buffer(16 * (n + 1))
+    lib().oracle_inv_cipher_trace(_buf(key), 8 * len(key), _buf(block), tr)
     return [tr.raw[16 * r:16 * r + 16] for r in range(n + 1)]
 
 

@@ -246,20 +246,31 @@ static void cipher_block(const uint8_t in[16], uint8_t out[16], const uint8_t *w
     store_state(out, &st);
 }
 
-static void inv_cipher_block(const uint8_t in[16], uint8_t out[16], const uint8_t *w, int nr) {
+/* trace (optional, 16*(nr+1) bytes): trace[0] = state after AddRoundKey(Nr);
+ * trace[i], 1 <= i <= Nr-1 = state after the loop iteration for round Nr-i
+ * (after InvMixColumns); trace[Nr] = output. */
+static void inv_cipher_block_t(const uint8_t in[16], uint8_t out[16], const uint8_t *w, int nr,
+                               uint8_t *trace) {
     state_t st;
     load_state(&st, in);
     add_round_key(&st, w, nr);
+    if (trace) store_state(trace, &st);
     for (int r = nr - 1; r >= 1; r--) {
         inv_shift_rows(&st);
         inv_sub_bytes(&st);
         add_round_key(&st, w, r);
         inv_mix_columns(&st);
+        if (trace) store_state(trace + 16 * (nr - r), &st);
     }
     inv_shift_rows(&st);
     inv_sub_bytes(&st);
     add_round_key(&st, w, 0);
+    if (trace) store_state(trace + 16 * nr, &st);
     store_state(out, &st);
+}
+
+static void inv_cipher_block(const uint8_t in[16], uint8_t out[16], const uint8_t *w, int nr) {
+    inv_cipher_block_t(in, out, w, nr, NULL);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -315,6 +326,15 @@ int oracle_cipher_trace(const uint8_t *key, int keybits, const uint8_t in[16], u
     int nr = oracle_key_expansion(key, keybits, w);
     if (nr <= 0) return -1;
     cipher_block(in, out, w, nr, trace);
+    return nr;
+}
+
+/* Per-iteration trace of one block through InvCipher (see inv_cipher_block_t). */
+int oracle_inv_cipher_trace(const uint8_t *key, int keybits, const uint8_t in[16], uint8_t *trace) {
+    uint8_t w[16 * 15], out[16];
+    int nr = oracle_key_expansion(key, keybits, w);
+    if (nr <= 0) return -1;
+    inv_cipher_block_t(in, out, w, nr, trace);
     return nr;
 }
 

@@ -190,6 +190,16 @@ def cbc_decrypt(rk: RoundKeys, iv: bytes, x, out=None, stream=None):
     return out
 
 
+def ecb_trace(rk: RoundKeys, x, rounds: int, decrypt: bool = False, out=None):
+    """aes_ecb_trace: state after ARK(0) + `rounds` rounds (round-by-round parity pin)."""
+    out = _prep_out(x, out)
+    with _on_device(x.device):
+        code = _native.lib.aes_ecb_trace(ctypes.byref(rk.c), rk.nr, int(bool(decrypt)), int(rounds), x.data_ptr(),
+                                         out.data_ptr(), x.numel() // 16, _raw_stream(x.device.index))
+    _check(code, "aes_ecb_trace")
+    return out
+
+
 class Pipeline:
     """Host-resident end-to-end path: aes_pipeline_create/run/destroy.
 

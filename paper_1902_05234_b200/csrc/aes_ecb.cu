@@ -181,50 +181,70 @@ struct Tab<V_CONST> {
 // ---------------------------------------------------------------------------
 // One block: Algorithm 1 (corrected, R1) with the Eq 26 round
 // ---------------------------------------------------------------------------
-template <int NR, bool DEC, class TB>
-__device__ __forceinline__ uint4 cipher_block(const TB& tb, uint4 v, const RK& rk) {
-    // A6: round-0 AddRoundKey (Eq 21)
-    uint32_t s0 = v.x ^ rk.w[0], s1 = v.y ^ rk.w[1], s2 = v.z ^ rk.w[2], s3 = v.w ^ rk.w[3];
-    // A7: rounds 1..NR-1, Eq 26
-#pragma unroll
-    for (int r = 1; r < NR; r++) {
-        uint32_t e0, e1, e2, e3;
-        if (!DEC) {
-            e0 = tb.t(0, s0, 0) ^ tb.t(1, s1, 1) ^ tb.t(2, s2, 2) ^ tb.t(3, s3, 3) ^ rk.w[4 * r + 0];
-            e1 = tb.t(0, s1, 0) ^ tb.t(1, s2, 1) ^ tb.t(2, s3, 2) ^ tb.t(3, s0, 3) ^ rk.w[4 * r + 1];
-            e2 = tb.t(0, s2, 0) ^ tb.t(1, s3, 1) ^ tb.t(2, s0, 2) ^ tb.t(3, s1, 3) ^ rk.w[4 * r + 2];
-            e3 = tb.t(0, s3, 0) ^ tb.t(1, s0, 1) ^ tb.t(2, s1, 2) ^ tb.t(3, s2, 3) ^ rk.w[4 * r + 3];
-        } else {
-            e0 = tb.t(0, s0, 0) ^ tb.t(1, s3, 1) ^ tb.t(2, s2, 2) ^ tb.t(3, s1, 3) ^ rk.w[4 * r + 0];
-            e1 = tb.t(0, s1, 0) ^ tb.t(1, s0, 1) ^ tb.t(2, s3, 2) ^ tb.t(3, s2, 3) ^ rk.w[4 * r + 1];
-            e2 = tb.t(0, s2, 0) ^ tb.t(1, s1, 1) ^ tb.t(2, s0, 2) ^ tb.t(3, s3, 3) ^ rk.w[4 * r + 2];
-            e3 = tb.t(0, s3, 0) ^ tb.t(1, s2, 1) ^ tb.t(2, s1, 2) ^ tb.t(3, s0, 3) ^ rk.w[4 * r + 3];
-        }
-        s0 = e0; s1 = e1; s2 = e2; s3 = e3;
+// A7: one Eq 26 round on the state (s0..s3) with round key k[0..3].
+// Encryption: e_j = T0[b0(s_j)] ^ T1[b1(s_{j+1})] ^ T2[b2(s_{j+2})] ^ T3[b3(s_{j+3})] ^ k_j.
+// Decryption (equivalent inverse, R12): Td tables with s_j, s_{j-1}, s_{j-2}, s_{j-3}.
+template <bool DEC, class TB, class K>
+__device__ __forceinline__ void t_round(const TB& tb, uint32_t& s0, uint32_t& s1, uint32_t& s2, uint32_t& s3,
+                                        const K& k) {
+    uint32_t e0, e1, e2, e3;
+    if (!DEC) {
+        e0 = tb.t(0, s0, 0) ^ tb.t(1, s1, 1) ^ tb.t(2, s2, 2) ^ tb.t(3, s3, 3) ^ k[0];
+        e1 = tb.t(0, s1, 0) ^ tb.t(1, s2, 1) ^ tb.t(2, s3, 2) ^ tb.t(3, s0, 3) ^ k[1];
+        e2 = tb.t(0, s2, 0) ^ tb.t(1, s3, 1) ^ tb.t(2, s0, 2) ^ tb.t(3, s1, 3) ^ k[2];
+        e3 = tb.t(0, s3, 0) ^ tb.t(1, s0, 1) ^ tb.t(2, s1, 2) ^ tb.t(3, s2, 3) ^ k[3];
+    } else {
+        e0 = tb.t(0, s0, 0) ^ tb.t(1, s3, 1) ^ tb.t(2, s2, 2) ^ tb.t(3, s1, 3) ^ k[0];
+        e1 = tb.t(0, s1, 0) ^ tb.t(1, s0, 1) ^ tb.t(2, s3, 2) ^ tb.t(3, s2, 3) ^ k[1];
+        e2 = tb.t(0, s2, 0) ^ tb.t(1, s1, 1) ^ tb.t(2, s0, 2) ^ tb.t(3, s3, 3) ^ k[2];
+        e3 = tb.t(0, s3, 0) ^ tb.t(1, s2, 1) ^ tb.t(2, s1, 2) ^ tb.t(3, s0, 3) ^ k[3];
     }
-    // A8: final round = SubBytes + ShiftRows + AddRoundKey (no MixColumns)
+    s0 = e0; s1 = e1; s2 = e2; s3 = e3;
+}
+
+// A8: final round = SubBytes + ShiftRows + AddRoundKey, no MixColumns (R1, R14).
+template <bool DEC, class TB, class K>
+__device__ __forceinline__ uint4 final_round(const TB& tb, uint32_t s0, uint32_t s1, uint32_t s2, uint32_t s3,
+                                             const K& k) {
     uint4 o;
     if (!DEC) {
         // S[x] sits in byte 0 of Te2, byte 1 of Te3, byte 2 of Te0, byte 3 of Te1
 #define AES_FINAL_E(a, b, c, d) \
     (((tb.t(2, a, 0) & 0x000000FFu) | (tb.t(3, b, 1) & 0x0000FF00u) | (tb.t(0, c, 2) & 0x00FF0000u) | \
       (tb.t(1, d, 3) & 0xFF000000u)))
-        o.x = AES_FINAL_E(s0, s1, s2, s3) ^ rk.w[4 * NR + 0];
-        o.y = AES_FINAL_E(s1, s2, s3, s0) ^ rk.w[4 * NR + 1];
-        o.z = AES_FINAL_E(s2, s3, s0, s1) ^ rk.w[4 * NR + 2];
-        o.w = AES_FINAL_E(s3, s0, s1, s2) ^ rk.w[4 * NR + 3];
+        o.x = AES_FINAL_E(s0, s1, s2, s3) ^ k[0];
+        o.y = AES_FINAL_E(s1, s2, s3, s0) ^ k[1];
+        o.z = AES_FINAL_E(s2, s3, s0, s1) ^ k[2];
+        o.w = AES_FINAL_E(s3, s0, s1, s2) ^ k[3];
 #undef AES_FINAL_E
     } else {
 #define AES_FINAL_D(a, b, c, d) \
     (((tb.si(a, 0) & 0x000000FFu) | (tb.si(b, 1) & 0x0000FF00u) | (tb.si(c, 2) & 0x00FF0000u) | \
       (tb.si(d, 3) & 0xFF000000u)))
-        o.x = AES_FINAL_D(s0, s3, s2, s1) ^ rk.w[4 * NR + 0];
-        o.y = AES_FINAL_D(s1, s0, s3, s2) ^ rk.w[4 * NR + 1];
-        o.z = AES_FINAL_D(s2, s1, s0, s3) ^ rk.w[4 * NR + 2];
-        o.w = AES_FINAL_D(s3, s2, s1, s0) ^ rk.w[4 * NR + 3];
+        o.x = AES_FINAL_D(s0, s3, s2, s1) ^ k[0];
+        o.y = AES_FINAL_D(s1, s0, s3, s2) ^ k[1];
+        o.z = AES_FINAL_D(s2, s1, s0, s3) ^ k[2];
+        o.w = AES_FINAL_D(s3, s2, s1, s0) ^ k[3];
 #undef AES_FINAL_D
     }
     return o;
+}
+
+// Round key r as an indexable view of the by-value parameter (constant bank).
+struct KeyAt {
+    const RK& rk;
+    int r;
+    __device__ __forceinline__ uint32_t operator[](int j) const { return rk.w[4 * r + j]; }
+};
+
+// One block: Algorithm 1 (corrected, R1) with the Eq 26 round.
+template <int NR, bool DEC, class TB>
+__device__ __forceinline__ uint4 cipher_block(const TB& tb, uint4 v, const RK& rk) {
+    // A6: round-0 AddRoundKey (Eq 21)
+    uint32_t s0 = v.x ^ rk.w[0], s1 = v.y ^ rk.w[1], s2 = v.z ^ rk.w[2], s3 = v.w ^ rk.w[3];
+#pragma unroll
+    for (int r = 1; r < NR; r++) t_round<DEC>(tb, s0, s1, s2, s3, KeyAt{rk, r});   // A7
+    return final_round<DEC>(tb, s0, s1, s2, s3, KeyAt{rk, NR});                    // A8
 }
 
 // ---------------------------------------------------------------------------
@@ -301,6 +321,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     cbc_decrypt_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n,
                        const __grid_constant__ RK rk, const __grid_constant__ ModeP mp) {
     aes_body<NR, true, V_REPL, 1, M_CBCD>(in, out, n, rk, mp);
+}
+
+// Debug/pin kernel (aes_ecb_trace): the state after ARK(0) and `rounds` rounds
+// of the SAME t_round / final_round code the production kernels inline, one
+// state per thread.  rounds = NR gives the full cipher.
+template <int NR, bool DEC>
+__global__ void __launch_bounds__(kThreads, 1)
+    trace_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n, const __grid_constant__ RK rk,
+                 int rounds) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    const Tab<V_REPL> tb = Tab<V_REPL>::template setup<DEC>(smem);
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += T) {
+        uint4 v = in[i];
+        uint32_t s0 = v.x ^ rk.w[0], s1 = v.y ^ rk.w[1], s2 = v.z ^ rk.w[2], s3 = v.w ^ rk.w[3];
+        for (int r = 1; r <= rounds && r < NR; r++) t_round<DEC>(tb, s0, s1, s2, s3, KeyAt{rk, r});
+        out[i] = rounds >= NR ? final_round<DEC>(tb, s0, s1, s2, s3, KeyAt{rk, NR}) : make_uint4(s0, s1, s2, s3);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -545,6 +583,35 @@ aes_status aes_cbc_decrypt(const aes_round_keys* rk, int nr, const uint8_t* iv, 
         m.iv[j] = (uint32_t)iv[4 * j] | ((uint32_t)iv[4 * j + 1] << 8) | ((uint32_t)iv[4 * j + 2] << 16) |
                   ((uint32_t)iv[4 * j + 3] << 24);
     return launch(rk, nr, 1, in, out, nblocks, (cudaStream_t)stream, nullptr, true, M_CBCD, &m);
+}
+
+aes_status aes_ecb_trace(const aes_round_keys* rk, int nr, int decrypt, int rounds, const void* in, void* out,
+                         uint64_t nblocks, void* stream) {
+    aes_status st = validate_keys(rk, nr);
+    if (st) return st;
+    if (rounds < 0 || rounds > nr) return AES_ERANGE;
+    if (nblocks == 0) return AES_OK;
+    if ((st = validate_buffers(in, out, nblocks))) return st;
+    int dev = 0, occ = 1, nsm = 148;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    if ((st = check_device_ptr(in, dev))) return st;
+    if (out != in && (st = check_device_ptr(out, dev))) return st;
+    const void* f;
+    if (nr == 10) f = decrypt ? (const void*)&trace_kernel<10, true> : (const void*)&trace_kernel<10, false>;
+    else if (nr == 12) f = decrypt ? (const void*)&trace_kernel<12, true> : (const void*)&trace_kernel<12, false>;
+    else f = decrypt ? (const void*)&trace_kernel<14, true> : (const void*)&trace_kernel<14, false>;
+    KernelInfo ki{f, decrypt ? kSmemReplDec : kSmemReplEnc};
+    if ((st = resident_ctas(dev, ki, &occ, &nsm))) return st;
+    uint64_t want = (nblocks + 31) / 32, cap = (uint64_t)nsm * occ;
+    RK k;
+    std::memcpy(k.w, decrypt ? rk->dk : rk->ek, sizeof k.w);
+    const uint4* pin = static_cast<const uint4*>(in);
+    uint4* pout = static_cast<uint4*>(out);
+    void* args[] = {(void*)&pin, (void*)&pout, (void*)&nblocks, (void*)&k, (void*)&rounds};
+    e = cudaLaunchKernel(f, dim3((unsigned)(want < cap ? want : cap)), dim3(kThreads), args, ki.smem,
+                         (cudaStream_t)stream);
+    return e == cudaSuccess ? AES_OK : cuda_fail(e);
 }
 
 aes_status aes_mb_lds_gather(void* sink, int grid, int iters, void* stream) {

@@ -171,3 +171,13 @@ def test_ctr_cbc_validation_errors():
     assert L.aes_cbc_decrypt(ctypes.byref(rk.c), 14, None, A, A + 4096, 4, None) == _native.AES_ENULL
     assert L.aes_cbc_decrypt(ctypes.byref(rk.c), 14, iv, A, A, 4, None) == _native.AES_EOVERLAP
     assert L.aes_cbc_decrypt(ctypes.byref(rk.c), 14, iv, A + 4, A + 4096, 4, None) == _native.AES_EALIGN
+
+
+def test_trace_validation():
+    from paper_1902_05234_b200 import _native
+    import paper_1902_05234_b200 as aes
+    rk = aes.expand_key(bytes(16))
+    L = _native.lib
+    assert L.aes_ecb_trace(ctypes.byref(rk.c), 10, 0, 11, 0x10000, 0x10000, 1, None) == _native.AES_ERANGE
+    assert L.aes_ecb_trace(ctypes.byref(rk.c), 10, 0, -1, 0x10000, 0x10000, 1, None) == _native.AES_ERANGE
+    assert L.aes_ecb_trace(ctypes.byref(rk.c), 10, 0, 3, 0x10000, 0x10000, 0, None) == _native.AES_OK

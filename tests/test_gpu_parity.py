@@ -335,3 +335,34 @@ def test_host_threads_call_concurrently(aes):
     for t, (key, ct, ok) in results.items():
         assert ok
         assert np.array_equal(ct, oracle.encrypt(key, host, nthreads=4)), t
+
+
+@pytest.mark.parametrize("keybits", [128, 192, 256])
+def test_round_by_round_trace_against_oracle(aes, keybits):
+    """SURVEY.md 8(c) per-round pin: after ARK(0) and r Eq-26 rounds the GPU
+    state equals the oracle's state after AddRoundKey(r) (encryption), and
+    the equivalent-inverse state after r rounds equals the straightforward
+    InvCipher's state after r iterations (decryption), for every r."""
+    key = synth.key(keybits)
+    rk = aes.expand_key(key)
+    n = 333
+    host = synth.blocks(11, n)
+    x = _dev_rand(n, first=11)
+    E = [oracle.cipher_trace(key, host[16 * i:16 * i + 16].tobytes()) for i in range(n)]
+    C = np.frombuffer(b"".join(e[-1] for e in E), np.uint8)
+    D = [oracle.inv_cipher_trace(key, C[16 * i:16 * i + 16].tobytes()) for i in range(n)]
+    tc = torch.from_numpy(C.copy()).cuda()
+    for r in range(rk.nr + 1):
+        ge = aes.ecb_trace(rk, x, r).cpu().numpy().tobytes()
+        assert ge == b"".join(e[r] for e in E), ("enc", keybits, r)
+        gd = aes.ecb_trace(rk, tc, r, decrypt=True).cpu().numpy().tobytes()
+        assert gd == b"".join(d[r] for d in D), ("dec", keybits, r)
+
+
+def test_round_trace_fips197_appendix_b(aes):
+    d = {ln.split()[0]: ln.split()[1] for ln in open(golden("fips197_appB.txt")) if ln.strip() and not ln.startswith("#")}
+    rk = aes.expand_key(bytes.fromhex(d["key"]))
+    x = torch.frombuffer(bytearray(bytes.fromhex(d["pt"])), dtype=torch.uint8).cuda()
+    for r in range(10):
+        assert aes.ecb_trace(rk, x, r).cpu().numpy().tobytes().hex() == d[f"r{r}"], r
+    assert aes.ecb_trace(rk, x, 10).cpu().numpy().tobytes().hex() == d["ct"]

@@ -339,3 +339,20 @@ def test_ctr_counter_wrap_offset_and_openssl():
         ct = e.update(data.tobytes()) + e.finalize()
         assert oracle.cbc(key, iv, data, False).tobytes() == ct
         assert oracle.cbc(key, iv, np.frombuffer(ct, np.uint8), True).tobytes() == data.tobytes()
+
+
+def test_inv_cipher_trace_mirrors_the_forward_trace():
+    """InvCipher's state after its iteration for round r equals
+    ShiftRows(SubBytes(E_{r-1})), E = the (App B-pinned) forward trace; the
+    last entry is the plaintext.  Checked for every key size."""
+    rng = np.random.default_rng(17)
+    for kb in (128, 192, 256):
+        for _ in range(20):
+            key = rng.integers(0, 256, kb // 8, dtype=np.uint8).tobytes()
+            p = rng.integers(0, 256, 16, dtype=np.uint8).tobytes()
+            E = oracle.cipher_trace(key, p)
+            nr = len(E) - 1
+            D = oracle.inv_cipher_trace(key, E[nr])
+            assert D[nr] == p
+            for i in range(nr):
+                assert D[i] == oracle.transform("shift_rows", oracle.transform("sub_bytes", E[nr - 1 - i])), (kb, i)
