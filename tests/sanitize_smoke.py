@@ -5,7 +5,7 @@ tiny grids.  Exit code 0 iff every output matches the oracle."""
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))  # repo root
 sys.path.insert(0, ROOT)
 import numpy as np
 import torch

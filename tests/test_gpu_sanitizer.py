@@ -19,7 +19,7 @@ def test_compute_sanitizer(tool):
     cmd = [cs, "--tool", tool, "--error-exitcode", "99"]
     if tool == "memcheck":
         cmd += ["--leak-check", "no"]
-    r = subprocess.run(cmd + [sys.executable, os.path.join(ROOT, "tools", "sanitize_smoke.py")],
+    r = subprocess.run(cmd + [sys.executable, os.path.join(ROOT, "tests", "sanitize_smoke.py")],
                        capture_output=True, text=True, timeout=1800, cwd=ROOT)
     tail = (r.stdout + r.stderr)[-3000:]
     assert r.returncode == 0, tail

@@ -9,8 +9,10 @@
   --what config3   config 3: AES-256 decrypt, 4 GiB
   --what ladder    the paper's file-size ladder (Tables 4-5), device-resident and e2e
 
-Every timed point is preceded by a parity check of that configuration against
-the oracle on sampled blocks.  Buffers smaller than 2x L2 are measured with an
+Every timed point is preceded by a parity check of that configuration: sampled
+blocks against tests/golden/samples.txt (expected values written by the oracle,
+tests/golden/make_samples.py) for the random stream, and against the default
+kernel (itself oracle-checked in tests/) for the other data kinds.  Buffers smaller than 2x L2 are measured with an
 L2 flush (a 512 MiB write) before every rep; larger ones are not.  JSONL on stdout.
 """
 from __future__ import annotations
@@ -27,9 +29,9 @@ sys.path.insert(0, ROOT)
 import numpy as np
 import torch
 
-import oracle
 import paper_1902_05234_b200 as aes
 import synth
+from synth import golden
 
 NR = {128: 10, 192: 12, 256: 14}
 
@@ -53,15 +55,16 @@ def lds_peak(s):
     return n / (e0.elapsed_time(e1) * 1e-3)
 
 
-def parity(key, x, out, decrypt, first=0, k=512):
-    n = x.numel() // 16
-    rng = np.random.default_rng(n)
-    idx = np.unique(np.r_[0, n - 1, rng.integers(0, n, k)]).astype(np.int64)
-    xin = x.view(-1, 16)[torch.from_numpy(idx).cuda()].cpu().numpy().reshape(-1)
-    want = oracle.ecb(key, xin, decrypt, nthreads=8)
-    got = out.view(-1, 16)[torch.from_numpy(idx).cuda()].cpu().numpy().reshape(-1)
-    if not np.array_equal(got, want):
-        raise SystemExit(f"PARITY FAILURE n={n} decrypt={decrypt}")
+def _gather(t):
+    return lambda loc: t.view(-1, 16)[torch.from_numpy(loc).cuda()].cpu().numpy()
+
+
+def parity(keybits, out, op):
+    """Sampled blocks of `out` (result of `op` on the random stream from block 0)
+    against the oracle-written golden samples."""
+    n = out.numel() // 16
+    if golden.check(op, keybits, 0, n, _gather(out)) < 1:
+        raise SystemExit(f"no golden samples for n={n}")
 
 
 def time_op(fn, s, reps, flush=None):
@@ -115,7 +118,7 @@ def sizes(a, s, hbm, ldsp):
                 f = (lambda: aes.ecb(rk, x, dec, out=out))
                 f()
                 torch.cuda.synchronize()
-                parity(key, x, out, dec)
+                parity(kb, out, "ecb_dec" if dec else "ecb_enc")
                 reps = 20 if nbytes < (4 << 30) else 5
                 warm = nbytes >= 2 * l2
                 for _ in range(3):
@@ -159,7 +162,10 @@ def variants(a, s, hbm, ldsp):
                 f = (lambda: aes.ecb(rk, x, dec, out=out, variant=v, states_per_thread=spt))
                 f()
                 torch.cuda.synchronize()
-                parity(key, x, out, dec)
+                if kind == "random":
+                    parity(128, out, "ecb_dec" if dec else "ecb_enc")
+                else:
+                    assert torch.equal(out, aes.ecb(rk, x, dec)), ("variant mismatch", v, spt, kind)
                 reps = 10 if v != 3 else 3
                 tmin, tmed = time_op(f, s, reps)
                 g = 8 * nbytes / tmin / 1e9
@@ -180,7 +186,7 @@ def config3(a, s, hbm, ldsp):
     f()
     torch.cuda.synchronize()
     assert torch.equal(out, x)
-    parity(key, ct, out, True)
+    parity(256, ct, "ecb_enc")
     for _ in range(3):
         f()
     torch.cuda.synchronize()   # warm-ups ran on the default stream; s is non-blocking
@@ -208,7 +214,7 @@ def ladder(a, s, hbm, ldsp):
             f = (lambda: aes.ecb(rk, x, dec, out=out))
             f()
             torch.cuda.synchronize()
-            parity(key, x, out, dec, k=64)
+            parity(128, out, "ecb_dec" if dec else "ecb_enc")
             tmin, tmed = time_op(f, s, 20, flush)
             import time
             pipe.run(rk, hx, ho, decrypt=dec)
@@ -241,18 +247,7 @@ def modes(a, s, hbm, ldsp):
                 f = (lambda: aes.cbc_decrypt(rk, iv, x, out=out))
             f()
             torch.cuda.synchronize()
-            rng = np.random.default_rng(kb)
-            idx = np.unique(np.r_[0, 1, n - 1, rng.integers(0, n, 256)]).astype(np.int64)
-            got = out.view(-1, 16)[torch.from_numpy(idx).cuda()].cpu().numpy()
-            if mode == "ctr":
-                for i, g in zip(idx, got):
-                    w = oracle.ctr(key, iv, x.view(-1, 16)[int(i)].cpu().numpy().copy(), block_offset=int(i))
-                    assert np.array_equal(g, w), ("ctr parity", i)
-            else:
-                for i, g in zip(idx, got):
-                    prev = iv if i == 0 else x.view(-1, 16)[int(i) - 1].cpu().numpy().tobytes()
-                    w = oracle.cbc(key, prev, x.view(-1, 16)[int(i)].cpu().numpy().copy(), True)
-                    assert np.array_equal(g, w), ("cbc parity", i)
+            parity(kb, out, "ctr" if mode == "ctr" else "cbc_dec")
             for _ in range(3):
                 f()
             torch.cuda.synchronize()   # warm-ups ran on the default stream; s is non-blocking
