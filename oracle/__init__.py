@@ -31,7 +31,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-fno-semantic-interposition", "-shared", "-pthread",
-                               "-o", tmp, _SRC])
+                               "-o", tmp, _SRC], stdout=subprocess.DEVNULL)
         os.replace(tmp, _LIB)
     return _LIB
 
