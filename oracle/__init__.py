@@ -26,13 +26,23 @@ _lock = threading.Lock()
 _lib = None
 
 
+def _digest() -> str:
+    import hashlib
+    with open(_SRC, "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()
+
+
 def build(force: bool = False) -> str:
-    """Compile liboracle.so with gcc (plain C, -O2, pthreads)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    """Compile liboracle.so with gcc (plain C, -O2, pthreads); content-hash staleness."""
+    stamp = _LIB + ".stamp"
+    stale = not os.path.exists(_LIB) or not os.path.exists(stamp) or open(stamp).read().strip() != _digest()
+    if force or stale:
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-fno-semantic-interposition", "-shared", "-pthread",
                                "-o", tmp, _SRC], stdout=subprocess.DEVNULL)
         os.replace(tmp, _LIB)
+        with open(stamp, "w") as f:
+            f.write(_digest())
     return _LIB
 
 
