@@ -115,6 +115,33 @@ aes_status aes_ctr_xcrypt(const aes_round_keys *rk, int nr, const uint8_t *iv, u
 aes_status aes_cbc_decrypt(const aes_round_keys *rk, int nr, const uint8_t *iv, const void *in, void *out,
                            uint64_t nblocks, void *stream);
 
+/* aes_ecb_batch: many messages, each with its own key, in one launch
+ * (ECB of Eq 1 applied per message; the paper's workloads are files of
+ * 1,202 .. 1,190,402 bytes, which one launch each would
+ * leave launch-bound).  Message i = segs[i]: nblocks 16-byte blocks read at
+ * in_base + in_offset and written at out_base + out_offset with round keys
+ * keys[key_index] (ek, or dk when decrypt = 1).
+ *  keys  : host array of nkeys round keys, all with the same nr (else AES_ENR).
+ *  segs  : host array of nsegs descriptors; read during the call only (they are
+ *          staged to the device in a stream-ordered allocation freed after the
+ *          kernel).  Offsets must be multiples of 16 (AES_EALIGN); a segment's
+ *          output must equal or be disjoint from its own input (AES_EOVERLAP);
+ *          outputs of DIFFERENT segments must not overlap other segments'
+ *          inputs or outputs (not checked: O(n^2)); empty segments are allowed.
+ *  in_base/out_base : device pointers of the current device, 16-byte aligned.
+ * Asynchronous on `stream`.  Errors: AES_ENULL, AES_ERANGE (nkeys < 1, key_index
+ * out of range, size overflow), AES_ENR, AES_EALIGN, AES_EOVERLAP,
+ * AES_ENOTDEVICE, AES_ECUDA. */
+typedef struct {
+    uint64_t in_offset;   /* bytes from in_base  */
+    uint64_t out_offset;  /* bytes from out_base */
+    uint64_t nblocks;
+    uint32_t key_index;
+    uint32_t reserved;
+} aes_segment;
+aes_status aes_ecb_batch(const aes_round_keys *keys, int nkeys, int decrypt, const aes_segment *segs, uint32_t nsegs,
+                         const void *in_base, void *out_base, void *stream);
+
 /* Kernel variants (T-table placement).  All variants
  * produce bit-identical output; they differ only in speed.
  *  AES_VAR_DEFAULT    : tuned choice (currently AES_VAR_SMEM_REPL).

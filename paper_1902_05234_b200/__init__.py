@@ -18,7 +18,8 @@ from . import _native
 from ._native import (AES_VAR_CONST, AES_VAR_DEFAULT, AES_VAR_SMEM_PLAIN, AES_VAR_SMEM_REPL,
                       aes_launch_config, aes_round_keys, status_string)
 
-__all__ = ["RoundKeys", "expand_key", "ecb_encrypt", "ecb_decrypt", "ecb", "ctr_xcrypt", "cbc_decrypt", "Pipeline",
+__all__ = ["RoundKeys", "expand_key", "ecb_encrypt", "ecb_decrypt", "ecb", "ecb_batch", "ctr_xcrypt", "cbc_decrypt",
+           "ecb_trace", "Pipeline",
            "lds_gather", "AesError", "AES_VAR_DEFAULT", "AES_VAR_SMEM_REPL", "AES_VAR_SMEM_PLAIN",
            "AES_VAR_CONST", "abi_version"]
 
@@ -188,6 +189,45 @@ def cbc_decrypt(rk: RoundKeys, iv: bytes, x, out=None, stream=None):
                                            x.numel() // 16, sp)
     _check(code, "aes_cbc_decrypt")
     return out
+
+
+def ecb_batch(rks, xs, outs=None, key_index=None, decrypt: bool = False, stream=None):
+    """aes_ecb_batch: ECB of many messages (each its own key) in ONE launch.
+
+    rks: list of RoundKeys (same key size); xs: list of contiguous CUDA uint8
+    tensors on one device (numel % 16 == 0, 16-byte aligned); key_index[i]
+    picks rks for xs[i] (default: i).  Returns the list of outputs (``outs``
+    if given; an output may be its own input)."""
+    import torch
+    n = len(xs)
+    if key_index is None:
+        key_index = list(range(n))
+    if len(key_index) != n or not rks:
+        raise ValueError("need one key index per message and at least one key")
+    if outs is None:
+        outs = [torch.empty_like(x) for x in xs]
+    if len(outs) != n:
+        raise ValueError("one output per message")
+    for x, o in zip(xs, outs):
+        _check_tensor(x, "x")
+        _check_tensor(o, "out")
+        if o.numel() != x.numel():
+            raise ValueError("out must match x")
+    if n == 0:
+        return outs
+    dev = xs[0].device
+    in_base = min(x.data_ptr() for x in xs)
+    out_base = min(o.data_ptr() for o in outs)
+    segs = (_native.aes_segment * n)()
+    for i, (x, o) in enumerate(zip(xs, outs)):
+        segs[i] = _native.aes_segment(x.data_ptr() - in_base, o.data_ptr() - out_base, x.numel() // 16,
+                                      int(key_index[i]), 0)
+    keys = (aes_round_keys * len(rks))(*[r.c for r in rks])
+    with _on_device(dev):
+        sp = stream.cuda_stream if stream is not None else _raw_stream(dev.index)
+        code = _native.lib.aes_ecb_batch(keys, len(rks), int(bool(decrypt)), segs, n, in_base, out_base, sp)
+    _check(code, "aes_ecb_batch")
+    return outs
 
 
 def ecb_trace(rk: RoundKeys, x, rounds: int, decrypt: bool = False, out=None):

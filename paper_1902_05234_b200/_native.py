@@ -19,13 +19,18 @@ AES_VAR_DEFAULT, AES_VAR_SMEM_REPL, AES_VAR_SMEM_PLAIN, AES_VAR_CONST = range(4)
 
 # every symbol include/aes_b200.h declares
 EXPORTS = ("aes_expand_key", "aes_ecb_encrypt", "aes_ecb_decrypt", "aes_ecb_launch",
-           "aes_ctr_xcrypt", "aes_cbc_decrypt", "aes_ecb_trace", "aes_pipeline_create", "aes_pipeline_run", "aes_pipeline_destroy",
+           "aes_ctr_xcrypt", "aes_cbc_decrypt", "aes_ecb_trace", "aes_ecb_batch", "aes_pipeline_create", "aes_pipeline_run", "aes_pipeline_destroy",
            "aes_mb_lds_gather", "aes_status_string", "aes_last_cuda_error", "aes_abi_version")
 
 
 class aes_round_keys(ctypes.Structure):
     _fields_ = [("ek", ctypes.c_uint32 * 60), ("dk", ctypes.c_uint32 * 60),
                 ("nr", ctypes.c_int32), ("keybits", ctypes.c_int32)]
+
+
+class aes_segment(ctypes.Structure):
+    _fields_ = [("in_offset", ctypes.c_uint64), ("out_offset", ctypes.c_uint64), ("nblocks", ctypes.c_uint64),
+                ("key_index", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
 class aes_launch_config(ctypes.Structure):
@@ -53,6 +58,8 @@ def _load():
     L.aes_cbc_decrypt.argtypes = [RKP, i32, ctypes.c_char_p, p, p, u64, p]
     L.aes_ecb_trace.restype = i32
     L.aes_ecb_trace.argtypes = [RKP, i32, i32, i32, p, p, u64, p]
+    L.aes_ecb_batch.restype = i32
+    L.aes_ecb_batch.argtypes = [RKP, i32, i32, ctypes.POINTER(aes_segment), ctypes.c_uint32, p, p, p]
     L.aes_pipeline_create.restype = i32
     L.aes_pipeline_create.argtypes = [u64, i32, ctypes.POINTER(p)]
     L.aes_pipeline_run.restype = i32

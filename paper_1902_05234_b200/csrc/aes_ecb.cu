@@ -30,6 +30,7 @@
 #include <cstdint>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "aes_b200.h"
 #include "aes_tables.h"
@@ -323,6 +324,56 @@ __global__ void __launch_bounds__(kThreads, 1)
     aes_body<NR, true, V_REPL, 1, M_CBCD>(in, out, n, rk, mp);
 }
 
+// ---------------------------------------------------------------------------
+// Batched multi-message ECB (aes_ecb_batch): many messages, each with its own
+// key, in ONE launch -- the paper's file-sized workloads at
+// bulk rate instead of one launch per file.  Segment s covers global blocks
+// [first, first + n); a warp's 32 consecutive global blocks find their
+// segment with one warp-uniform binary search (broadcast loads) plus a short
+// forward walk; round keys are read per round from the (L1-resident)
+// descriptor area: a broadcast when the warp is inside one message.
+// ---------------------------------------------------------------------------
+struct BatchSeg {
+    uint64_t in_off, out_off;   // byte offsets from in_base / out_base
+    uint64_t first, n;          // global block range
+    uint32_t key, pad;          // index into the key words (60 per key)
+};
+
+struct KeyPtrAt {
+    const uint32_t* p;  // round key r of this message
+    __device__ __forceinline__ uint32_t operator[](int j) const { return __ldg(p + j); }
+};
+
+template <int NR, bool DEC>
+__global__ void __launch_bounds__(kThreads, 1)
+    batch_kernel(const char* __restrict__ in_base, char* __restrict__ out_base, const BatchSeg* __restrict__ segs,
+                 uint32_t nsegs, uint64_t total, const uint32_t* __restrict__ keyw) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    const Tab<V_REPL> tb = Tab<V_REPL>::template setup<DEC>(smem);
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i - lane < total; i += T) {
+        const uint64_t g0 = i - lane;                 // warp-uniform
+        uint32_t lo = 0, hi = nsegs - 1;              // last segment with first <= g0
+        while (lo < hi) {
+            uint32_t mid = (lo + hi + 1) >> 1;
+            if (__ldg(&segs[mid].first) <= g0) lo = mid; else hi = mid - 1;
+        }
+        if (i >= total) continue;
+        uint32_t sidx = lo;
+        while (i >= __ldg(&segs[sidx].first) + __ldg(&segs[sidx].n)) sidx++;
+        const BatchSeg* sg = segs + sidx;
+        const uint64_t local = i - __ldg(&sg->first);
+        const uint32_t* kp = keyw + 60u * __ldg(&sg->key);
+        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(in_base + __ldg(&sg->in_off)) + local);
+        uint32_t s0 = v.x ^ __ldg(kp), s1 = v.y ^ __ldg(kp + 1), s2 = v.z ^ __ldg(kp + 2), s3 = v.w ^ __ldg(kp + 3);
+#pragma unroll
+        for (int r = 1; r < NR; r++) t_round<DEC>(tb, s0, s1, s2, s3, KeyPtrAt{kp + 4 * r});
+        __stcs(reinterpret_cast<uint4*>(out_base + __ldg(&sg->out_off)) + local,
+               final_round<DEC>(tb, s0, s1, s2, s3, KeyPtrAt{kp + 4 * NR}));
+    }
+}
+
 // Debug/pin kernel (aes_ecb_trace): the state after ARK(0) and `rounds` rounds
 // of the SAME t_round / final_round code the production kernels inline, one
 // state per thread.  rounds = NR gives the full cipher.
@@ -612,6 +663,72 @@ aes_status aes_ecb_trace(const aes_round_keys* rk, int nr, int decrypt, int roun
     e = cudaLaunchKernel(f, dim3((unsigned)(want < cap ? want : cap)), dim3(kThreads), args, ki.smem,
                          (cudaStream_t)stream);
     return e == cudaSuccess ? AES_OK : cuda_fail(e);
+}
+
+aes_status aes_ecb_batch(const aes_round_keys* keys, int nkeys, int decrypt, const aes_segment* segs, uint32_t nsegs,
+                         const void* in_base, void* out_base, void* stream) {
+    if (!keys) return AES_ENULL;
+    if (nkeys < 1) return AES_ERANGE;
+    const int nr = keys[0].nr;
+    for (int k = 0; k < nkeys; k++) {
+        aes_status st = validate_keys(&keys[k], nr);
+        if (st) return st;
+    }
+    if (nsegs == 0) return AES_OK;
+    if (!segs || !in_base || !out_base) return AES_ENULL;
+    if (((uintptr_t)in_base | (uintptr_t)out_base) & 15) return AES_EALIGN;
+    std::vector<BatchSeg> hs(nsegs);
+    uint64_t total = 0;
+    for (uint32_t i = 0; i < nsegs; i++) {
+        const aes_segment& a = segs[i];
+        if (a.key_index >= (uint32_t)nkeys) return AES_ERANGE;
+        if ((a.in_offset | a.out_offset) & 15) return AES_EALIGN;
+        if (a.nblocks > (UINT64_MAX >> 4) || total + a.nblocks < total) return AES_ERANGE;
+        uint64_t bytes = a.nblocks << 4;
+        uintptr_t pi = (uintptr_t)in_base + a.in_offset, po = (uintptr_t)out_base + a.out_offset;
+        if (pi < (uintptr_t)in_base || po < (uintptr_t)out_base || pi > UINTPTR_MAX - bytes || po > UINTPTR_MAX - bytes)
+            return AES_ERANGE;
+        if (pi != po && pi < po + bytes && po < pi + bytes) return AES_EOVERLAP;
+        hs[i] = BatchSeg{a.in_offset, a.out_offset, total, a.nblocks, a.key_index, 0};
+        total += a.nblocks;
+    }
+    if (total == 0) return AES_OK;
+    int dev = 0, occ = 1, nsm = 148;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    aes_status st;
+    if ((st = check_device_ptr(in_base, dev))) return st;
+    if (out_base != in_base && (st = check_device_ptr(out_base, dev))) return st;
+    const void* f = nullptr;
+    if (nr == 10) f = decrypt ? (const void*)&batch_kernel<10, true> : (const void*)&batch_kernel<10, false>;
+    else if (nr == 12) f = decrypt ? (const void*)&batch_kernel<12, true> : (const void*)&batch_kernel<12, false>;
+    else f = decrypt ? (const void*)&batch_kernel<14, true> : (const void*)&batch_kernel<14, false>;
+    KernelInfo ki{f, decrypt ? kSmemReplDec : kSmemReplEnc};
+    if ((st = resident_ctas(dev, ki, &occ, &nsm))) return st;
+    // descriptors: segments, then 60 key words per key (ek or dk), in one
+    // stream-ordered allocation that is freed after the kernel on `stream`
+    const size_t seg_bytes = sizeof(BatchSeg) * nsegs, key_bytes = 240ull * nkeys;
+    std::vector<char> host(seg_bytes + key_bytes);
+    std::memcpy(host.data(), hs.data(), seg_bytes);
+    for (int k = 0; k < nkeys; k++)
+        std::memcpy(host.data() + seg_bytes + 240ull * k, decrypt ? keys[k].dk : keys[k].ek, 240);
+    cudaStream_t cs = (cudaStream_t)stream;
+    void* d = nullptr;
+    if ((e = cudaMallocAsync(&d, host.size(), cs)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaMemcpyAsync(d, host.data(), host.size(), cudaMemcpyHostToDevice, cs)) != cudaSuccess) {
+        cudaFreeAsync(d, cs);
+        return cuda_fail(e);
+    }
+    const char* pin = static_cast<const char*>(in_base);
+    char* pout = static_cast<char*>(out_base);
+    const BatchSeg* dsegs = static_cast<const BatchSeg*>(d);
+    const uint32_t* dkeys = reinterpret_cast<const uint32_t*>(static_cast<char*>(d) + seg_bytes);
+    void* args[] = {(void*)&pin, (void*)&pout, (void*)&dsegs, (void*)&nsegs, (void*)&total, (void*)&dkeys};
+    uint64_t want = (total + 31) / 32, cap = (uint64_t)nsm * occ;
+    e = cudaLaunchKernel(f, dim3((unsigned)(want < cap ? want : cap)), dim3(kThreads), args, ki.smem, cs);
+    cudaError_t e2 = cudaFreeAsync(d, cs);
+    if (e != cudaSuccess) return cuda_fail(e);
+    return e2 == cudaSuccess ? AES_OK : cuda_fail(e2);
 }
 
 aes_status aes_mb_lds_gather(void* sink, int grid, int iters, void* stream) {

@@ -181,3 +181,27 @@ def test_trace_validation():
     assert L.aes_ecb_trace(ctypes.byref(rk.c), 10, 0, 11, 0x10000, 0x10000, 1, None) == _native.AES_ERANGE
     assert L.aes_ecb_trace(ctypes.byref(rk.c), 10, 0, -1, 0x10000, 0x10000, 1, None) == _native.AES_ERANGE
     assert L.aes_ecb_trace(ctypes.byref(rk.c), 10, 0, 3, 0x10000, 0x10000, 0, None) == _native.AES_OK
+
+
+def test_batch_validation():
+    from paper_1902_05234_b200 import _native
+    import paper_1902_05234_b200 as aes
+    L = _native.lib
+    k128 = aes.expand_key(bytes(16)).c
+    k256 = aes.expand_key(bytes(32)).c
+    keys = (_native.aes_round_keys * 2)(k128, k128)
+    seg = (_native.aes_segment * 2)(_native.aes_segment(0, 0, 4, 0, 0), _native.aes_segment(64, 64, 4, 1, 0))
+    A = 0x10000
+    assert L.aes_ecb_batch(None, 1, 0, seg, 2, A, A, None) == _native.AES_ENULL
+    assert L.aes_ecb_batch(keys, 0, 0, seg, 2, A, A, None) == _native.AES_ERANGE
+    assert L.aes_ecb_batch(keys, 2, 0, seg, 0, None, None, None) == _native.AES_OK
+    assert L.aes_ecb_batch(keys, 2, 0, None, 2, A, A, None) == _native.AES_ENULL
+    mixed = (_native.aes_round_keys * 2)(k128, k256)
+    assert L.aes_ecb_batch(mixed, 2, 0, seg, 2, A, A, None) == _native.AES_ENR
+    bad_key = (_native.aes_segment * 1)(_native.aes_segment(0, 0, 4, 2, 0))
+    assert L.aes_ecb_batch(keys, 2, 0, bad_key, 1, A, A, None) == _native.AES_ERANGE
+    mis = (_native.aes_segment * 1)(_native.aes_segment(8, 8, 4, 0, 0))
+    assert L.aes_ecb_batch(keys, 2, 0, mis, 1, A, A, None) == _native.AES_EALIGN
+    ovl = (_native.aes_segment * 1)(_native.aes_segment(0, 16, 4, 0, 0))
+    assert L.aes_ecb_batch(keys, 2, 0, ovl, 1, A, A, None) == _native.AES_EOVERLAP
+    assert L.aes_ecb_batch(keys, 2, 0, seg, 2, A + 8, A, None) == _native.AES_EALIGN

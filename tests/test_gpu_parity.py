@@ -366,3 +366,44 @@ def test_round_trace_fips197_appendix_b(aes):
     for r in range(10):
         assert aes.ecb_trace(rk, x, r).cpu().numpy().tobytes().hex() == d[f"r{r}"], r
     assert aes.ecb_trace(rk, x, 10).cpu().numpy().tobytes().hex() == d["ct"]
+
+
+@pytest.mark.parametrize("keybits", [128, 192, 256])
+@pytest.mark.parametrize("decrypt", [False, True])
+def test_batch_many_messages_many_keys_against_oracle(aes, keybits, decrypt):
+    """aes_ecb_batch: messages of the paper's file sizes (PAPER.md:509-518,
+    ceil(size/16) blocks) plus empty / 1-block / ragged ones, each with its
+    own key, some in place; every output byte checked against the oracle."""
+    rng = np.random.default_rng(keybits + int(decrypt))
+    ladder = [76, 291, 582, 1163, 2326, 4651, 9301, 18601, 37201, 74401]
+    sizes = ladder + [0, 1, 2, 31, 32, 33] + [int(v) for v in rng.integers(1, 3000, 40)]
+    rng.shuffle(sizes)
+    nkeys = 7
+    keys = [rng.integers(0, 256, keybits // 8, dtype=np.uint8).tobytes() for _ in range(nkeys)]
+    rks = [aes.expand_key(k) for k in keys]
+    kidx = [int(v) for v in rng.integers(0, nkeys, len(sizes))]
+    xs, hosts = [], []
+    first = 0
+    for n in sizes:
+        h = synth.blocks(first, n)
+        first += n
+        hosts.append(h)
+        xs.append(torch.from_numpy(h.copy()).cuda())
+    outs = [x if i % 5 == 0 else None for i, x in enumerate(xs)]      # every 5th in place
+    outs = [o if o is not None else torch.empty_like(x) for o, x in zip(outs, xs)]
+    got = aes.ecb_batch(rks, xs, outs, key_index=kidx, decrypt=decrypt)
+    torch.cuda.synchronize()
+    for i, (g, h) in enumerate(zip(got, hosts)):
+        want = oracle.ecb(keys[kidx[i]], h, decrypt, nthreads=4)
+        assert np.array_equal(g.cpu().numpy(), want), (i, sizes[i])
+
+
+def test_batch_thousand_small_files_one_launch(aes):
+    key = synth.key(128)
+    rk = aes.expand_key(key)
+    n = 76   # 1,202-byte file of Table 4, padded to whole blocks
+    base = _dev_rand(1000 * n)
+    xs = [base[16 * n * i:16 * n * (i + 1)] for i in range(1000)]
+    outs = aes.ecb_batch([rk], xs, key_index=[0] * 1000)
+    got = torch.cat(outs).cpu().numpy()
+    assert np.array_equal(got, oracle.encrypt(key, synth.blocks(0, 1000 * n), nthreads=8))
