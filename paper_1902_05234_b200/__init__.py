@@ -18,7 +18,7 @@ from . import _native
 from ._native import (AES_VAR_CONST, AES_VAR_DEFAULT, AES_VAR_SMEM_PLAIN, AES_VAR_SMEM_REPL,
                       aes_launch_config, aes_round_keys, status_string)
 
-__all__ = ["RoundKeys", "expand_key", "ecb_encrypt", "ecb_decrypt", "ecb", "ecb_batch", "ctr_xcrypt", "cbc_decrypt",
+__all__ = ["RoundKeys", "expand_key", "ecb_encrypt", "ecb_decrypt", "ecb", "ecb_batch", "ecb_batch_offsets", "ctr_xcrypt", "cbc_decrypt",
            "ecb_trace", "Pipeline",
            "lds_gather", "AesError", "AES_VAR_DEFAULT", "AES_VAR_SMEM_REPL", "AES_VAR_SMEM_PLAIN",
            "AES_VAR_CONST", "abi_version"]
@@ -191,6 +191,27 @@ def cbc_decrypt(rk: RoundKeys, iv: bytes, x, out=None, stream=None):
     return out
 
 
+def ecb_batch_offsets(rks, in_base: int, out_base: int, in_offsets, out_offsets, nblocks, key_index,
+                      decrypt: bool = False, device=None, stream=None):
+    """aes_ecb_batch over raw device addresses: message i = nblocks[i] blocks at
+    in_base + in_offsets[i] -> out_base + out_offsets[i] with rks[key_index[i]].
+    Array arguments are vectors of equal length (numpy or lists); no per-message
+    Python work beyond packing them."""
+    import numpy as np
+    import torch
+    m = len(nblocks)
+    segs = np.zeros(m, dtype=[("in", "<u8"), ("out", "<u8"), ("n", "<u8"), ("k", "<u4"), ("r", "<u4")])
+    segs["in"], segs["out"], segs["n"], segs["k"] = in_offsets, out_offsets, nblocks, key_index
+    keys = (aes_round_keys * len(rks))(*[r.c for r in rks])
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    with _on_device(dev):
+        sp = stream.cuda_stream if stream is not None else _raw_stream(dev.index)
+        code = _native.lib.aes_ecb_batch(keys, len(rks), int(bool(decrypt)),
+                                         segs.ctypes.data_as(ctypes.POINTER(_native.aes_segment)), m,
+                                         in_base, out_base, sp)
+    _check(code, "aes_ecb_batch")
+
+
 def ecb_batch(rks, xs, outs=None, key_index=None, decrypt: bool = False, stream=None):
     """aes_ecb_batch: ECB of many messages (each its own key) in ONE launch.
 
@@ -213,20 +234,14 @@ def ecb_batch(rks, xs, outs=None, key_index=None, decrypt: bool = False, stream=
         _check_tensor(o, "out")
         if o.numel() != x.numel():
             raise ValueError("out must match x")
-    if n == 0:
+    live = [i for i in range(n) if xs[i].numel()]
+    if not live:
         return outs
-    dev = xs[0].device
-    in_base = min(x.data_ptr() for x in xs)
-    out_base = min(o.data_ptr() for o in outs)
-    segs = (_native.aes_segment * n)()
-    for i, (x, o) in enumerate(zip(xs, outs)):
-        segs[i] = _native.aes_segment(x.data_ptr() - in_base, o.data_ptr() - out_base, x.numel() // 16,
-                                      int(key_index[i]), 0)
-    keys = (aes_round_keys * len(rks))(*[r.c for r in rks])
-    with _on_device(dev):
-        sp = stream.cuda_stream if stream is not None else _raw_stream(dev.index)
-        code = _native.lib.aes_ecb_batch(keys, len(rks), int(bool(decrypt)), segs, n, in_base, out_base, sp)
-    _check(code, "aes_ecb_batch")
+    ip = [xs[i].data_ptr() for i in live]
+    op = [outs[i].data_ptr() for i in live]
+    ib, ob = min(ip), min(op)
+    ecb_batch_offsets(rks, ib, ob, [p - ib for p in ip], [p - ob for p in op], [xs[i].numel() // 16 for i in live],
+                      [key_index[i] for i in live], decrypt, xs[live[0]].device, stream)
     return outs
 
 

@@ -274,7 +274,10 @@ def batch(a, s, hbm, ldsp):
         xs = [base[16 * nb * i:16 * nb * (i + 1)] for i in range(M)]
         os_ = [out[16 * nb * i:16 * nb * (i + 1)] for i in range(M)]
         kidx = [i % 64 for i in range(M)]
-        fbatch = (lambda: aes.ecb_batch(rks, xs, os_, key_index=kidx))
+        offs = np.arange(M, dtype=np.uint64) * np.uint64(16 * nb)
+        nbs = np.full(M, nb, dtype=np.uint64)
+        kid = np.array(kidx, dtype=np.uint32)
+        fbatch = (lambda: aes.ecb_batch_offsets(rks, base.data_ptr(), out.data_ptr(), offs, offs, nbs, kid))
         fbatch()
         torch.cuda.synchronize()
         # parity: message i under key i % 64 -- check message 0 and 1 against the
