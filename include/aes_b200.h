@@ -121,7 +121,8 @@ aes_status aes_cbc_decrypt(const aes_round_keys *rk, int nr, const uint8_t *iv, 
  * leave launch-bound).  Message i = segs[i]: nblocks 16-byte blocks read at
  * in_base + in_offset and written at out_base + out_offset with round keys
  * keys[key_index] (ek, or dk when decrypt = 1).
- *  keys  : host array of nkeys round keys, all with the same nr (else AES_ENR).
+ *  keys  : host array of 1..128 round keys (staged in shared memory), all
+ *          with the same nr (else AES_ENR).
  *  segs  : host array of nsegs descriptors; read during the call only (they are
  *          staged to the device in a stream-ordered allocation freed after the
  *          kernel).  Offsets must be multiples of 16 (AES_EALIGN); a segment's
@@ -129,7 +130,7 @@ aes_status aes_cbc_decrypt(const aes_round_keys *rk, int nr, const uint8_t *iv, 
  *          outputs of DIFFERENT segments must not overlap other segments'
  *          inputs or outputs (not checked: O(n^2)); empty segments are allowed.
  *  in_base/out_base : device pointers of the current device, 16-byte aligned.
- * Asynchronous on `stream`.  Errors: AES_ENULL, AES_ERANGE (nkeys < 1, key_index
+ * Asynchronous on `stream`.  Errors: AES_ENULL, AES_ERANGE (nkeys not in 1..128, key_index
  * out of range, size overflow), AES_ENR, AES_EALIGN, AES_EOVERLAP,
  * AES_ENOTDEVICE, AES_ECUDA. */
 typedef struct {

@@ -339,38 +339,56 @@ struct BatchSeg {
     uint32_t key, pad;          // index into the key words (60 per key)
 };
 
-struct KeyPtrAt {
-    const uint32_t* p;  // round key r of this message
-    __device__ __forceinline__ uint32_t operator[](int j) const { return __ldg(p + j); }
+struct KeyVec {
+    uint4 k;   // one round key, fetched with a single LDS.128 (a broadcast within a message)
+    __device__ __forceinline__ uint32_t operator[](int j) const { return j == 0 ? k.x : j == 1 ? k.y : j == 2 ? k.z : k.w; }
 };
 
+constexpr int kBatchMaxKeys = 128;   // 128 x 240 B = 30 KiB of key schedules staged in shared memory
+
+// Each CTA owns one contiguous range of global blocks; its 1024 threads walk it
+// 1024 consecutive blocks per trip, so the segment of a warp only moves
+// forward: found once by a warp-uniform binary search, then advanced by a
+// short forward walk (broadcast loads).
 template <int NR, bool DEC>
 __global__ void __launch_bounds__(kThreads, 1)
     batch_kernel(const char* __restrict__ in_base, char* __restrict__ out_base, const BatchSeg* __restrict__ segs,
-                 uint32_t nsegs, uint64_t total, const uint32_t* __restrict__ keyw) {
+                 uint32_t nsegs, uint64_t total, const uint32_t* __restrict__ keyw, int nkeys) {
     extern __shared__ __align__(16) uint32_t smem[];
-    const Tab<V_REPL> tb = Tab<V_REPL>::template setup<DEC>(smem);
-    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    const Tab<V_REPL> tb = Tab<V_REPL>::template setup<DEC>(smem);   // ends with __syncthreads
+    uint32_t* skeys = smem + (DEC ? kSmemReplDec : kSmemReplEnc) / 4;
+    for (int w = threadIdx.x; w < 60 * nkeys; w += blockDim.x) skeys[w] = __ldg(keyw + w);
+    __syncthreads();
+    const uint64_t per = (total + gridDim.x - 1) / gridDim.x;
+    const uint64_t c0 = per * blockIdx.x, c1 = c0 + per < total ? c0 + per : total;
     const uint32_t lane = threadIdx.x & 31;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i - lane < total; i += T) {
-        const uint64_t g0 = i - lane;                 // warp-uniform
-        uint32_t lo = 0, hi = nsegs - 1;              // last segment with first <= g0
-        while (lo < hi) {
-            uint32_t mid = (lo + hi + 1) >> 1;
-            if (__ldg(&segs[mid].first) <= g0) lo = mid; else hi = mid - 1;
+    uint32_t seg = 0;
+    bool found = false;
+    for (uint64_t w0 = c0 + (threadIdx.x & ~31u); w0 < c1; w0 += blockDim.x) {   // w0: warp-uniform
+        if (!found) {                                  // last segment with first <= w0
+            uint32_t lo = 0, hi = nsegs - 1;
+            while (lo < hi) {
+                uint32_t mid = (lo + hi + 1) >> 1;
+                if (__ldg(&segs[mid].first) <= w0) lo = mid; else hi = mid - 1;
+            }
+            seg = lo;
+            found = true;
         }
-        if (i >= total) continue;
-        uint32_t sidx = lo;
+        while (w0 >= __ldg(&segs[seg].first) + __ldg(&segs[seg].n)) seg++;   // warp-uniform advance
+        const uint64_t i = w0 + lane;
+        if (i >= c1) continue;
+        uint32_t sidx = seg;
         while (i >= __ldg(&segs[sidx].first) + __ldg(&segs[sidx].n)) sidx++;
         const BatchSeg* sg = segs + sidx;
         const uint64_t local = i - __ldg(&sg->first);
-        const uint32_t* kp = keyw + 60u * __ldg(&sg->key);
+        const uint4* kp = reinterpret_cast<const uint4*>(skeys + 60u * __ldg(&sg->key));
         const uint4 v = __ldcs(reinterpret_cast<const uint4*>(in_base + __ldg(&sg->in_off)) + local);
-        uint32_t s0 = v.x ^ __ldg(kp), s1 = v.y ^ __ldg(kp + 1), s2 = v.z ^ __ldg(kp + 2), s3 = v.w ^ __ldg(kp + 3);
+        const uint4 k0 = kp[0];
+        uint32_t s0 = v.x ^ k0.x, s1 = v.y ^ k0.y, s2 = v.z ^ k0.z, s3 = v.w ^ k0.w;
 #pragma unroll
-        for (int r = 1; r < NR; r++) t_round<DEC>(tb, s0, s1, s2, s3, KeyPtrAt{kp + 4 * r});
+        for (int r = 1; r < NR; r++) t_round<DEC>(tb, s0, s1, s2, s3, KeyVec{kp[r]});
         __stcs(reinterpret_cast<uint4*>(out_base + __ldg(&sg->out_off)) + local,
-               final_round<DEC>(tb, s0, s1, s2, s3, KeyPtrAt{kp + 4 * NR}));
+               final_round<DEC>(tb, s0, s1, s2, s3, KeyVec{kp[NR]}));
     }
 }
 
@@ -668,7 +686,7 @@ aes_status aes_ecb_trace(const aes_round_keys* rk, int nr, int decrypt, int roun
 aes_status aes_ecb_batch(const aes_round_keys* keys, int nkeys, int decrypt, const aes_segment* segs, uint32_t nsegs,
                          const void* in_base, void* out_base, void* stream) {
     if (!keys) return AES_ENULL;
-    if (nkeys < 1) return AES_ERANGE;
+    if (nkeys < 1 || nkeys > kBatchMaxKeys) return AES_ERANGE;
     const int nr = keys[0].nr;
     for (int k = 0; k < nkeys; k++) {
         aes_status st = validate_keys(&keys[k], nr);
@@ -703,8 +721,9 @@ aes_status aes_ecb_batch(const aes_round_keys* keys, int nkeys, int decrypt, con
     if (nr == 10) f = decrypt ? (const void*)&batch_kernel<10, true> : (const void*)&batch_kernel<10, false>;
     else if (nr == 12) f = decrypt ? (const void*)&batch_kernel<12, true> : (const void*)&batch_kernel<12, false>;
     else f = decrypt ? (const void*)&batch_kernel<14, true> : (const void*)&batch_kernel<14, false>;
-    KernelInfo ki{f, decrypt ? kSmemReplDec : kSmemReplEnc};
+    KernelInfo ki{f, (decrypt ? kSmemReplDec : kSmemReplEnc) + 240 * kBatchMaxKeys};
     if ((st = resident_ctas(dev, ki, &occ, &nsm))) return st;
+    const size_t smem = (decrypt ? kSmemReplDec : kSmemReplEnc) + 240ull * nkeys;
     // descriptors: segments, then 60 key words per key (ek or dk), in one
     // stream-ordered allocation that is freed after the kernel on `stream`
     const size_t seg_bytes = sizeof(BatchSeg) * nsegs, key_bytes = 240ull * nkeys;
@@ -723,9 +742,10 @@ aes_status aes_ecb_batch(const aes_round_keys* keys, int nkeys, int decrypt, con
     char* pout = static_cast<char*>(out_base);
     const BatchSeg* dsegs = static_cast<const BatchSeg*>(d);
     const uint32_t* dkeys = reinterpret_cast<const uint32_t*>(static_cast<char*>(d) + seg_bytes);
-    void* args[] = {(void*)&pin, (void*)&pout, (void*)&dsegs, (void*)&nsegs, (void*)&total, (void*)&dkeys};
+    void* args[] = {(void*)&pin, (void*)&pout, (void*)&dsegs, (void*)&nsegs, (void*)&total, (void*)&dkeys,
+                    (void*)&nkeys};
     uint64_t want = (total + 31) / 32, cap = (uint64_t)nsm * occ;
-    e = cudaLaunchKernel(f, dim3((unsigned)(want < cap ? want : cap)), dim3(kThreads), args, ki.smem, cs);
+    e = cudaLaunchKernel(f, dim3((unsigned)(want < cap ? want : cap)), dim3(kThreads), args, smem, cs);
     cudaError_t e2 = cudaFreeAsync(d, cs);
     if (e != cudaSuccess) return cuda_fail(e);
     return e2 == cudaSuccess ? AES_OK : cuda_fail(e2);

@@ -194,6 +194,8 @@ def test_batch_validation():
     A = 0x10000
     assert L.aes_ecb_batch(None, 1, 0, seg, 2, A, A, None) == _native.AES_ENULL
     assert L.aes_ecb_batch(keys, 0, 0, seg, 2, A, A, None) == _native.AES_ERANGE
+    many = (_native.aes_round_keys * 129)(*([k128] * 129))
+    assert L.aes_ecb_batch(many, 129, 0, seg, 2, A, A, None) == _native.AES_ERANGE
     assert L.aes_ecb_batch(keys, 2, 0, seg, 0, None, None, None) == _native.AES_OK
     assert L.aes_ecb_batch(keys, 2, 0, None, 2, A, A, None) == _native.AES_ENULL
     mixed = (_native.aes_round_keys * 2)(k128, k256)
