@@ -18,7 +18,7 @@ from . import _native
 from ._native import (AES_VAR_CONST, AES_VAR_DEFAULT, AES_VAR_SMEM_PLAIN, AES_VAR_SMEM_REPL,
                       aes_launch_config, aes_round_keys, status_string)
 
-__all__ = ["RoundKeys", "expand_key", "ecb_encrypt", "ecb_decrypt", "ecb", "ecb_batch", "ecb_batch_offsets", "ctr_xcrypt", "cbc_decrypt",
+__all__ = ["RoundKeys", "expand_key", "ecb_encrypt", "ecb_decrypt", "ecb", "ecb_batch", "ecb_batch_offsets", "KeySet", "ctr_xcrypt", "cbc_decrypt",
            "ecb_trace", "Pipeline",
            "lds_gather", "AesError", "AES_VAR_DEFAULT", "AES_VAR_SMEM_REPL", "AES_VAR_SMEM_PLAIN",
            "AES_VAR_CONST", "abi_version"]
@@ -191,22 +191,40 @@ def cbc_decrypt(rk: RoundKeys, iv: bytes, x, out=None, stream=None):
     return out
 
 
+class KeySet:
+    """A fixed list of RoundKeys packed once as the C array aes_ecb_batch takes."""
+
+    __slots__ = ("arr", "n")
+
+    def __init__(self, rks):
+        self.n = len(rks)
+        self.arr = (aes_round_keys * self.n)(*[r.c for r in rks])
+
+
+_SEG_DTYPE = None
+
+
 def ecb_batch_offsets(rks, in_base: int, out_base: int, in_offsets, out_offsets, nblocks, key_index,
                       decrypt: bool = False, device=None, stream=None):
     """aes_ecb_batch over raw device addresses: message i = nblocks[i] blocks at
     in_base + in_offsets[i] -> out_base + out_offsets[i] with rks[key_index[i]].
-    Array arguments are vectors of equal length (numpy or lists); no per-message
-    Python work beyond packing them."""
+    ``rks``: a KeySet (cheapest) or a list of RoundKeys.  Array arguments are
+    vectors of equal length (numpy or lists); no per-message Python work beyond
+    packing them."""
     import numpy as np
     import torch
+    global _SEG_DTYPE
+    if _SEG_DTYPE is None:
+        _SEG_DTYPE = np.dtype([("in", "<u8"), ("out", "<u8"), ("n", "<u8"), ("k", "<u4"), ("r", "<u4")])
     m = len(nblocks)
-    segs = np.zeros(m, dtype=[("in", "<u8"), ("out", "<u8"), ("n", "<u8"), ("k", "<u4"), ("r", "<u4")])
-    segs["in"], segs["out"], segs["n"], segs["k"] = in_offsets, out_offsets, nblocks, key_index
-    keys = (aes_round_keys * len(rks))(*[r.c for r in rks])
+    segs = np.empty(m, dtype=_SEG_DTYPE)
+    segs["in"], segs["out"], segs["n"], segs["k"], segs["r"] = in_offsets, out_offsets, nblocks, key_index, 0
+    ks = rks if isinstance(rks, KeySet) else KeySet(rks)
+    keys = ks.arr
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     with _on_device(dev):
         sp = stream.cuda_stream if stream is not None else _raw_stream(dev.index)
-        code = _native.lib.aes_ecb_batch(keys, len(rks), int(bool(decrypt)),
+        code = _native.lib.aes_ecb_batch(keys, ks.n, int(bool(decrypt)),
                                          segs.ctypes.data_as(ctypes.POINTER(_native.aes_segment)), m,
                                          in_base, out_base, sp)
     _check(code, "aes_ecb_batch")

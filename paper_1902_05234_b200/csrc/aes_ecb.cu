@@ -362,33 +362,51 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t per = (total + gridDim.x - 1) / gridDim.x;
     const uint64_t c0 = per * blockIdx.x, c1 = c0 + per < total ? c0 + per : total;
     const uint32_t lane = threadIdx.x & 31;
-    uint32_t seg = 0;
-    bool found = false;
-    for (uint64_t w0 = c0 + (threadIdx.x & ~31u); w0 < c1; w0 += blockDim.x) {   // w0: warp-uniform
-        if (!found) {                                  // last segment with first <= w0
-            uint32_t lo = 0, hi = nsegs - 1;
-            while (lo < hi) {
-                uint32_t mid = (lo + hi + 1) >> 1;
-                if (__ldg(&segs[mid].first) <= w0) lo = mid; else hi = mid - 1;
-            }
-            seg = lo;
-            found = true;
+    uint64_t w0 = c0 + (threadIdx.x & ~31u);   // warp-uniform start of this warp's 32 blocks
+    if (w0 >= c1) return;                       // (no barriers below)
+    uint32_t seg;
+    {   // last segment with first <= w0: warp-uniform binary search (broadcast loads)
+        uint32_t lo = 0, hi = nsegs - 1;
+        while (lo < hi) {
+            uint32_t mid = (lo + hi + 1) >> 1;
+            if (__ldg(&segs[mid].first) <= w0) lo = mid; else hi = mid - 1;
         }
-        while (w0 >= __ldg(&segs[seg].first) + __ldg(&segs[seg].n)) seg++;   // warp-uniform advance
-        const uint64_t i = w0 + lane;
-        if (i >= c1) continue;
+        seg = lo;
+    }
+    // Software pipeline: the segment walk and the 128-bit load of the NEXT trip
+    // are issued before the rounds of the current one, hiding their latency chain.
+    bool have = false;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    uint4* op = nullptr;
+    const uint4* kp = nullptr;
+    auto fetch = [&](uint64_t base) {
+        while (base >= __ldg(&segs[seg].first) + __ldg(&segs[seg].n)) seg++;   // warp-uniform advance
+        const uint64_t i = base + lane;
+        have = i < c1;
+        if (!have) return;
         uint32_t sidx = seg;
         while (i >= __ldg(&segs[sidx].first) + __ldg(&segs[sidx].n)) sidx++;
         const BatchSeg* sg = segs + sidx;
         const uint64_t local = i - __ldg(&sg->first);
-        const uint4* kp = reinterpret_cast<const uint4*>(skeys + 60u * __ldg(&sg->key));
-        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(in_base + __ldg(&sg->in_off)) + local);
-        const uint4 k0 = kp[0];
-        uint32_t s0 = v.x ^ k0.x, s1 = v.y ^ k0.y, s2 = v.z ^ k0.z, s3 = v.w ^ k0.w;
+        v = __ldcs(reinterpret_cast<const uint4*>(in_base + __ldg(&sg->in_off)) + local);
+        op = reinterpret_cast<uint4*>(out_base + __ldg(&sg->out_off)) + local;
+        kp = reinterpret_cast<const uint4*>(skeys + 60u * __ldg(&sg->key));
+    };
+    fetch(w0);
+    while (w0 < c1) {
+        const bool chave = have;
+        const uint4 cv = v;
+        uint4* const cop = op;
+        const uint4* const ckp = kp;
+        w0 += blockDim.x;
+        if (w0 < c1) fetch(w0);
+        if (chave) {
+            const uint4 k0 = ckp[0];
+            uint32_t s0 = cv.x ^ k0.x, s1 = cv.y ^ k0.y, s2 = cv.z ^ k0.z, s3 = cv.w ^ k0.w;
 #pragma unroll
-        for (int r = 1; r < NR; r++) t_round<DEC>(tb, s0, s1, s2, s3, KeyVec{kp[r]});
-        __stcs(reinterpret_cast<uint4*>(out_base + __ldg(&sg->out_off)) + local,
-               final_round<DEC>(tb, s0, s1, s2, s3, KeyVec{kp[NR]}));
+            for (int r = 1; r < NR; r++) t_round<DEC>(tb, s0, s1, s2, s3, KeyVec{ckp[r]});
+            __stcs(cop, final_round<DEC>(tb, s0, s1, s2, s3, KeyVec{ckp[NR]}));
+        }
     }
 }
 

@@ -277,7 +277,8 @@ def batch(a, s, hbm, ldsp):
         offs = np.arange(M, dtype=np.uint64) * np.uint64(16 * nb)
         nbs = np.full(M, nb, dtype=np.uint64)
         kid = np.array(kidx, dtype=np.uint32)
-        fbatch = (lambda: aes.ecb_batch_offsets(rks, base.data_ptr(), out.data_ptr(), offs, offs, nbs, kid))
+        kset = aes.KeySet(rks)
+        fbatch = (lambda: aes.ecb_batch_offsets(kset, base.data_ptr(), out.data_ptr(), offs, offs, nbs, kid))
         fbatch()
         torch.cuda.synchronize()
         # parity: message i under key i % 64 -- check message 0 and 1 against the
@@ -288,6 +289,7 @@ def batch(a, s, hbm, ldsp):
             fbatch()
         torch.cuda.synchronize()
         tb, _ = time_op(fbatch, s, 10)
+        tbd = time_b2b(fbatch, s, 10)          # back to back: device-bound rate
         # M separate calls, back to back (host launch path included, as a user would see it)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -298,6 +300,7 @@ def batch(a, s, hbm, ldsp):
         tc = time.perf_counter() - t0
         payload = 16 * nb * M
         record(what="batch", file_bytes=fb, blocks_per_file=nb, files=M, batch_t_s=tb, batch_GBps=payload / tb / 1e9,
+               batch_b2b_t_s=tbd, batch_b2b_GBps=payload / tbd / 1e9,
                per_call_t_s=tc, per_call_GBps=payload / tc / 1e9, speedup=tc / tb,
                lds_frac=160 * nb * M / tb / ldsp)
 
