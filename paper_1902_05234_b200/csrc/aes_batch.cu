@@ -1,0 +1,173 @@
+// aes_batch.cu -- batched multi-message ECB (aes_ecb_batch): many messages,
+// each with its own key, in one launch (DESIGN.md section 11 "Batched small messages").
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "aes_b200.h"
+#include "aes_device.cuh"
+#include "aes_host.h"
+
+namespace aesb200 {
+
+// ---------------------------------------------------------------------------
+// Batched multi-message ECB (aes_ecb_batch): many messages, each with its own
+// key, in ONE launch -- the paper's file-sized workloads at
+// bulk rate instead of one launch per file.  Segment s covers global blocks
+// [first, first + n); a warp's 32 consecutive global blocks find their
+// segment with one warp-uniform binary search (broadcast loads) plus a short
+// forward walk; round keys are read per round from the (L1-resident)
+// descriptor area: a broadcast when the warp is inside one message.
+// ---------------------------------------------------------------------------
+struct BatchSeg {
+    uint64_t in_off, out_off;   // byte offsets from in_base / out_base
+    uint64_t first, n;          // global block range
+    uint32_t key, pad;          // index into the key words (60 per key)
+};
+
+struct KeyVec {
+    uint4 k;   // one round key, fetched with a single LDS.128 (a broadcast within a message)
+    __device__ __forceinline__ uint32_t operator[](int j) const { return j == 0 ? k.x : j == 1 ? k.y : j == 2 ? k.z : k.w; }
+};
+
+constexpr int kBatchMaxKeys = 128;   // 128 x 240 B = 30 KiB of key schedules staged in shared memory
+
+// Each CTA owns one contiguous range of global blocks; its 1024 threads walk it
+// 1024 consecutive blocks per trip, so the segment of a warp only moves
+// forward: found once by a warp-uniform binary search, then advanced by a
+// short forward walk (broadcast loads).
+template <int NR, bool DEC>
+__global__ void __launch_bounds__(kThreads, 1)
+    batch_kernel(const char* __restrict__ in_base, char* __restrict__ out_base, const BatchSeg* __restrict__ segs,
+                 uint32_t nsegs, uint64_t total, const uint32_t* __restrict__ keyw, int nkeys) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    const Tab<V_REPL> tb = Tab<V_REPL>::template setup<DEC>(smem);   // ends with __syncthreads
+    uint32_t* skeys = smem + (DEC ? kSmemReplDec : kSmemReplEnc) / 4;
+    for (int w = threadIdx.x; w < 60 * nkeys; w += blockDim.x) skeys[w] = __ldg(keyw + w);
+    __syncthreads();
+    const uint64_t per = (total + gridDim.x - 1) / gridDim.x;
+    const uint64_t c0 = per * blockIdx.x, c1 = c0 + per < total ? c0 + per : total;
+    const uint32_t lane = threadIdx.x & 31;
+    uint64_t w0 = c0 + (threadIdx.x & ~31u);   // warp-uniform start of this warp's 32 blocks
+    if (w0 >= c1) return;                       // (no barriers below)
+    uint32_t seg;
+    {   // last segment with first <= w0: warp-uniform binary search (broadcast loads)
+        uint32_t lo = 0, hi = nsegs - 1;
+        while (lo < hi) {
+            uint32_t mid = (lo + hi + 1) >> 1;
+            if (__ldg(&segs[mid].first) <= w0) lo = mid; else hi = mid - 1;
+        }
+        seg = lo;
+    }
+    // Software pipeline: the segment walk and the 128-bit load of the NEXT trip
+    // are issued before the rounds of the current one, hiding their latency chain.
+    bool have = false;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    uint4* op = nullptr;
+    const uint4* kp = nullptr;
+    auto fetch = [&](uint64_t base) {
+        while (base >= __ldg(&segs[seg].first) + __ldg(&segs[seg].n)) seg++;   // warp-uniform advance
+        const uint64_t i = base + lane;
+        have = i < c1;
+        if (!have) return;
+        uint32_t sidx = seg;
+        while (i >= __ldg(&segs[sidx].first) + __ldg(&segs[sidx].n)) sidx++;
+        const BatchSeg* sg = segs + sidx;
+        const uint64_t local = i - __ldg(&sg->first);
+        v = __ldcs(reinterpret_cast<const uint4*>(in_base + __ldg(&sg->in_off)) + local);
+        op = reinterpret_cast<uint4*>(out_base + __ldg(&sg->out_off)) + local;
+        kp = reinterpret_cast<const uint4*>(skeys + 60u * __ldg(&sg->key));
+    };
+    fetch(w0);
+    while (w0 < c1) {
+        const bool chave = have;
+        const uint4 cv = v;
+        uint4* const cop = op;
+        const uint4* const ckp = kp;
+        w0 += blockDim.x;
+        if (w0 < c1) fetch(w0);
+        if (chave) {
+            const uint4 k0 = ckp[0];
+            uint32_t s0 = cv.x ^ k0.x, s1 = cv.y ^ k0.y, s2 = cv.z ^ k0.z, s3 = cv.w ^ k0.w;
+#pragma unroll
+            for (int r = 1; r < NR; r++) t_round<DEC>(tb, s0, s1, s2, s3, KeyVec{ckp[r]});
+            __stcs(cop, final_round<DEC>(tb, s0, s1, s2, s3, KeyVec{ckp[NR]}));
+        }
+    }
+}
+
+}  // namespace aesb200
+
+using namespace aesb200;
+
+extern "C" aes_status aes_ecb_batch(const aes_round_keys* keys, int nkeys, int decrypt, const aes_segment* segs, uint32_t nsegs,
+                         const void* in_base, void* out_base, void* stream) {
+    if (!keys) return AES_ENULL;
+    if (nkeys < 1 || nkeys > kBatchMaxKeys) return AES_ERANGE;
+    const int nr = keys[0].nr;
+    for (int k = 0; k < nkeys; k++) {
+        aes_status st = validate_keys(&keys[k], nr);
+        if (st) return st;
+    }
+    if (nsegs == 0) return AES_OK;
+    if (!segs || !in_base || !out_base) return AES_ENULL;
+    if (((uintptr_t)in_base | (uintptr_t)out_base) & 15) return AES_EALIGN;
+    std::vector<BatchSeg> hs(nsegs);
+    uint64_t total = 0;
+    for (uint32_t i = 0; i < nsegs; i++) {
+        const aes_segment& a = segs[i];
+        if (a.key_index >= (uint32_t)nkeys) return AES_ERANGE;
+        if ((a.in_offset | a.out_offset) & 15) return AES_EALIGN;
+        if (a.nblocks > (UINT64_MAX >> 4) || total + a.nblocks < total) return AES_ERANGE;
+        uint64_t bytes = a.nblocks << 4;
+        uintptr_t pi = (uintptr_t)in_base + a.in_offset, po = (uintptr_t)out_base + a.out_offset;
+        if (pi < (uintptr_t)in_base || po < (uintptr_t)out_base || pi > UINTPTR_MAX - bytes || po > UINTPTR_MAX - bytes)
+            return AES_ERANGE;
+        if (pi != po && pi < po + bytes && po < pi + bytes) return AES_EOVERLAP;
+        hs[i] = BatchSeg{a.in_offset, a.out_offset, total, a.nblocks, a.key_index, 0};
+        total += a.nblocks;
+    }
+    if (total == 0) return AES_OK;
+    int dev = 0, occ = 1, nsm = 148;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    aes_status st;
+    if ((st = check_device_ptr(in_base, dev))) return st;
+    if (out_base != in_base && (st = check_device_ptr(out_base, dev))) return st;
+    const void* f = nullptr;
+    if (nr == 10) f = decrypt ? (const void*)&batch_kernel<10, true> : (const void*)&batch_kernel<10, false>;
+    else if (nr == 12) f = decrypt ? (const void*)&batch_kernel<12, true> : (const void*)&batch_kernel<12, false>;
+    else f = decrypt ? (const void*)&batch_kernel<14, true> : (const void*)&batch_kernel<14, false>;
+    KernelInfo ki{f, (decrypt ? kSmemReplDec : kSmemReplEnc) + 240 * kBatchMaxKeys};
+    if ((st = resident_ctas(dev, ki, &occ, &nsm))) return st;
+    const size_t smem = (decrypt ? kSmemReplDec : kSmemReplEnc) + 240ull * nkeys;
+    // descriptors: segments, then 60 key words per key (ek or dk), in one
+    // stream-ordered allocation that is freed after the kernel on `stream`
+    const size_t seg_bytes = sizeof(BatchSeg) * nsegs, key_bytes = 240ull * nkeys;
+    std::vector<char> host(seg_bytes + key_bytes);
+    std::memcpy(host.data(), hs.data(), seg_bytes);
+    for (int k = 0; k < nkeys; k++)
+        std::memcpy(host.data() + seg_bytes + 240ull * k, decrypt ? keys[k].dk : keys[k].ek, 240);
+    cudaStream_t cs = (cudaStream_t)stream;
+    cudaMemPool_t pool;
+    if ((st = desc_pool(dev, &pool))) return st;
+    void* d = nullptr;
+    if ((e = cudaMallocFromPoolAsync(&d, host.size(), pool, cs)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaMemcpyAsync(d, host.data(), host.size(), cudaMemcpyHostToDevice, cs)) != cudaSuccess) {
+        cudaFreeAsync(d, cs);
+        return cuda_fail(e);
+    }
+    const char* pin = static_cast<const char*>(in_base);
+    char* pout = static_cast<char*>(out_base);
+    const BatchSeg* dsegs = static_cast<const BatchSeg*>(d);
+    const uint32_t* dkeys = reinterpret_cast<const uint32_t*>(static_cast<char*>(d) + seg_bytes);
+    void* args[] = {(void*)&pin, (void*)&pout, (void*)&dsegs, (void*)&nsegs, (void*)&total, (void*)&dkeys,
+                    (void*)&nkeys};
+    uint64_t want = (total + 31) / 32, cap = (uint64_t)nsm * occ;
+    e = cudaLaunchKernel(f, dim3((unsigned)(want < cap ? want : cap)), dim3(kThreads), args, smem, cs);
+    cudaError_t e2 = cudaFreeAsync(d, cs);
+    if (e != cudaSuccess) return cuda_fail(e);
+    return e2 == cudaSuccess ? AES_OK : cuda_fail(e2);
+}

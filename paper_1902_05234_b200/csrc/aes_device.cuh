@@ -1,0 +1,250 @@
+// aes_device.cuh -- device building blocks shared by every kernel TU of
+// libaes_b200.so: compile-time table images (A3), the shared-memory table
+// policies (A4), the Eq 26 round and the final round (A6-A8).
+//
+//
+// One 16-byte state per thread (sec 4.1), held in four
+// 32-bit registers (column c = LE word c).  Rounds are the paper's T-table
+// round, Eq 26:
+//     e_j = T0[p_{0,j}] ^ T1[p_{1,j+1}] ^ T2[p_{2,j+2}] ^ T3[p_{3,j+3}] ^ k_j
+// with column indices mod 4 (R8), and for decryption the
+// equivalent-inverse round with Td0..Td3 and offsets j, j-1, j-2, j-3 (R12).
+// The final round (no MixColumns, R1) takes S[x] from a byte of a Te word
+// (R14) and Si[x] from a replicated Si word table.
+//
+// B200 design:
+//  * T-tables are lane-replicated in shared memory: entry x of table i for
+//    lane L lives at byte x*256 + (i&1)*128 + L*4 of region (i>>1), so every
+//    lane always hits bank L -- conflict-free for any data.  The address is
+//    ONE PRMT: __byte_perm(L*4, s, 0x1140 + 16k) = (byte k of s)<<8 | L*4;
+//    the table base is the LDS immediate.  The paper put the tables in
+//    __constant__ memory; that is kept as AES_VAR_CONST for the
+//    ablation, together with an unreplicated shared-memory variant.
+//  * Round keys are a by-value kernel parameter (constant bank, broadcast),
+//    as the paper's "round keys in the constant memory" but
+//    per launch, hence safe across concurrent streams.
+//  * States move as coalesced 128-bit streaming loads/stores (LDG.128/STG.128
+//    with evict-first hints); persistent grid-stride CTAs amortise the
+//    per-CTA table fill.  No tensor cores: this is table lookup, not a
+//    contraction (SURVEY.md 7 "Hard parts" 9).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "aes_host.h"
+#include "aes_tables.h"
+
+namespace aesb200 {
+
+// ---------------------------------------------------------------------------
+// Table images (compile time) in global and constant memory
+// ---------------------------------------------------------------------------
+struct Tables4 {
+    uint32_t te[4][256];   // Te0..Te3 (Eqs 22-25)
+    uint32_t td[4][256];   // Td0..Td3
+    uint32_t si4[256];     // Si[x] replicated in all four bytes
+};
+
+constexpr uint32_t rotl32(uint32_t v, int n) { return n ? (v << n) | (v >> (32 - n)) : v; }
+
+constexpr Tables4 build_tables4() {
+    Tables4 t{};
+    for (int i = 0; i < 4; i++)
+        for (int x = 0; x < 256; x++) {
+            t.te[i][x] = rotl32(kTables.te0[x], 8 * i);
+            t.td[i][x] = rotl32(kTables.td0[x], 8 * i);
+        }
+    for (int x = 0; x < 256; x++) t.si4[x] = 0x01010101u * kTables.si[x];
+    return t;
+}
+
+constexpr Tables4 kTables4 = build_tables4();
+static_assert(kTables4.te[1][0] == 0x6363C6A5u, "Te1 = rotl(Te0, 8)");
+
+static __device__ const Tables4 g_tab = kTables4;     // L2-resident source of the smem fill
+static __constant__ Tables4 c_tab = kTables4;         // AES_VAR_CONST (the paper's placement)
+
+struct RK {
+    uint32_t w[60];
+};
+
+
+// Replicated layout (bytes).  Region C (Si4) is only used by decryption.
+constexpr uint32_t kRegion = 65536;
+__host__ __device__ constexpr uint32_t off_t(int i) { return (uint32_t)(i >> 1) * kRegion + (uint32_t)(i & 1) * 128u; }
+constexpr uint32_t kOffSi = 2 * kRegion;
+constexpr size_t kSmemReplEnc = 2 * kRegion;
+constexpr size_t kSmemReplDec = 2 * kRegion + 255 * 256 + 128;
+constexpr size_t kSmemPlain = (4 * 256 + 256) * 4;
+
+enum { V_REPL = 1, V_PLAIN = 2, V_CONST = 3 };
+
+// ---------------------------------------------------------------------------
+// Table access policies: t(i, s, k) = T_i[byte k of s];  si(s, k) = Si4[byte k of s]
+// ---------------------------------------------------------------------------
+template <int V>
+struct Tab;
+
+template <>
+struct Tab<V_REPL> {
+    const char* sb;
+    uint32_t lo;  // lane*4 in byte 0
+    __device__ __forceinline__ uint32_t t(int i, uint32_t s, int k) const {
+        return *reinterpret_cast<const uint32_t*>(sb + off_t(i) + __byte_perm(lo, s, 0x1140 + 16 * k));
+    }
+    __device__ __forceinline__ uint32_t si(uint32_t s, int k) const {
+        return *reinterpret_cast<const uint32_t*>(sb + kOffSi + __byte_perm(lo, s, 0x1140 + 16 * k));
+    }
+    template <bool DEC>
+    __device__ __forceinline__ static Tab setup(uint32_t* smem) {
+        const uint32_t* src = DEC ? &g_tab.td[0][0] : &g_tab.te[0][0];
+        uint4* s4 = reinterpret_cast<uint4*>(smem);
+        // regions A,B: 32768 words; word w -> x = (w>>6)&255, table i = 2*(w>>14) + ((w>>5)&1)
+        // blockDim.x == kThreads: fixed trip counts, fully unrolled so every
+        // (L2-resident) table load of a thread is in flight at once
+        uint32_t v[8192 / kThreads];
+#pragma unroll
+        for (int it = 0; it < 8192 / kThreads; it++) {
+            int w = 4 * (threadIdx.x + it * kThreads);
+            int x = (w >> 6) & 255, i = 2 * (w >> 14) + ((w >> 5) & 1);
+            v[it] = __ldg(src + i * 256 + x);
+        }
+#pragma unroll
+        for (int it = 0; it < 8192 / kThreads; it++)
+            s4[threadIdx.x + it * kThreads] = make_uint4(v[it], v[it], v[it], v[it]);
+        if (DEC) {
+#pragma unroll
+            for (int it = 0; it < 2048 / kThreads; it++) {
+                int q = threadIdx.x + it * kThreads;
+                int x = q >> 3, part = q & 7;
+                uint32_t u = __ldg(g_tab.si4 + x);
+                s4[(kOffSi + x * 256) / 16 + part] = make_uint4(u, u, u, u);
+            }
+        }
+        __syncthreads();
+        Tab tb;
+        tb.sb = reinterpret_cast<const char*>(smem);
+        tb.lo = (threadIdx.x & 31) * 4;
+        return tb;
+    }
+};
+
+template <>
+struct Tab<V_PLAIN> {
+    const uint32_t* sm;
+    __device__ __forceinline__ uint32_t t(int i, uint32_t s, int k) const {
+        return sm[i * 256 + ((s >> (8 * k)) & 255)];
+    }
+    __device__ __forceinline__ uint32_t si(uint32_t s, int k) const {
+        return sm[1024 + ((s >> (8 * k)) & 255)];
+    }
+    template <bool DEC>
+    __device__ __forceinline__ static Tab setup(uint32_t* smem) {
+        const uint32_t* src = DEC ? &g_tab.td[0][0] : &g_tab.te[0][0];
+        for (int w = threadIdx.x; w < 1024; w += blockDim.x) smem[w] = src[w];
+        for (int w = threadIdx.x; w < 256; w += blockDim.x) smem[1024 + w] = g_tab.si4[w];
+        __syncthreads();
+        Tab tb;
+        tb.sm = smem;
+        return tb;
+    }
+};
+
+template <bool DEC>
+struct ConstSel;
+template <>
+struct ConstSel<false> {
+    __device__ __forceinline__ static uint32_t get(int i, uint32_t x) { return c_tab.te[i][x]; }
+};
+template <>
+struct ConstSel<true> {
+    __device__ __forceinline__ static uint32_t get(int i, uint32_t x) { return c_tab.td[i][x]; }
+};
+
+template <>
+struct Tab<V_CONST> {
+    bool dec;
+    __device__ __forceinline__ uint32_t t(int i, uint32_t s, int k) const {
+        uint32_t x = (s >> (8 * k)) & 255;
+        return dec ? ConstSel<true>::get(i, x) : ConstSel<false>::get(i, x);
+    }
+    __device__ __forceinline__ uint32_t si(uint32_t s, int k) const { return c_tab.si4[(s >> (8 * k)) & 255]; }
+    template <bool DEC>
+    __device__ __forceinline__ static Tab setup(uint32_t*) {
+        Tab tb;
+        tb.dec = DEC;
+        return tb;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// One block: Algorithm 1 (corrected, R1) with the Eq 26 round
+// ---------------------------------------------------------------------------
+// A7: one Eq 26 round on the state (s0..s3) with round key k[0..3].
+// Encryption: e_j = T0[b0(s_j)] ^ T1[b1(s_{j+1})] ^ T2[b2(s_{j+2})] ^ T3[b3(s_{j+3})] ^ k_j.
+// Decryption (equivalent inverse, R12): Td tables with s_j, s_{j-1}, s_{j-2}, s_{j-3}.
+template <bool DEC, class TB, class K>
+__device__ __forceinline__ void t_round(const TB& tb, uint32_t& s0, uint32_t& s1, uint32_t& s2, uint32_t& s3,
+                                        const K& k) {
+    uint32_t e0, e1, e2, e3;
+    if (!DEC) {
+        e0 = tb.t(0, s0, 0) ^ tb.t(1, s1, 1) ^ tb.t(2, s2, 2) ^ tb.t(3, s3, 3) ^ k[0];
+        e1 = tb.t(0, s1, 0) ^ tb.t(1, s2, 1) ^ tb.t(2, s3, 2) ^ tb.t(3, s0, 3) ^ k[1];
+        e2 = tb.t(0, s2, 0) ^ tb.t(1, s3, 1) ^ tb.t(2, s0, 2) ^ tb.t(3, s1, 3) ^ k[2];
+        e3 = tb.t(0, s3, 0) ^ tb.t(1, s0, 1) ^ tb.t(2, s1, 2) ^ tb.t(3, s2, 3) ^ k[3];
+    } else {
+        e0 = tb.t(0, s0, 0) ^ tb.t(1, s3, 1) ^ tb.t(2, s2, 2) ^ tb.t(3, s1, 3) ^ k[0];
+        e1 = tb.t(0, s1, 0) ^ tb.t(1, s0, 1) ^ tb.t(2, s3, 2) ^ tb.t(3, s2, 3) ^ k[1];
+        e2 = tb.t(0, s2, 0) ^ tb.t(1, s1, 1) ^ tb.t(2, s0, 2) ^ tb.t(3, s3, 3) ^ k[2];
+        e3 = tb.t(0, s3, 0) ^ tb.t(1, s2, 1) ^ tb.t(2, s1, 2) ^ tb.t(3, s0, 3) ^ k[3];
+    }
+    s0 = e0; s1 = e1; s2 = e2; s3 = e3;
+}
+
+// A8: final round = SubBytes + ShiftRows + AddRoundKey, no MixColumns (R1, R14).
+template <bool DEC, class TB, class K>
+__device__ __forceinline__ uint4 final_round(const TB& tb, uint32_t s0, uint32_t s1, uint32_t s2, uint32_t s3,
+                                             const K& k) {
+    uint4 o;
+    if (!DEC) {
+        // S[x] sits in byte 0 of Te2, byte 1 of Te3, byte 2 of Te0, byte 3 of Te1
+#define AES_FINAL_E(a, b, c, d) \
+    (((tb.t(2, a, 0) & 0x000000FFu) | (tb.t(3, b, 1) & 0x0000FF00u) | (tb.t(0, c, 2) & 0x00FF0000u) | \
+      (tb.t(1, d, 3) & 0xFF000000u)))
+        o.x = AES_FINAL_E(s0, s1, s2, s3) ^ k[0];
+        o.y = AES_FINAL_E(s1, s2, s3, s0) ^ k[1];
+        o.z = AES_FINAL_E(s2, s3, s0, s1) ^ k[2];
+        o.w = AES_FINAL_E(s3, s0, s1, s2) ^ k[3];
+#undef AES_FINAL_E
+    } else {
+#define AES_FINAL_D(a, b, c, d) \
+    (((tb.si(a, 0) & 0x000000FFu) | (tb.si(b, 1) & 0x0000FF00u) | (tb.si(c, 2) & 0x00FF0000u) | \
+      (tb.si(d, 3) & 0xFF000000u)))
+        o.x = AES_FINAL_D(s0, s3, s2, s1) ^ k[0];
+        o.y = AES_FINAL_D(s1, s0, s3, s2) ^ k[1];
+        o.z = AES_FINAL_D(s2, s1, s0, s3) ^ k[2];
+        o.w = AES_FINAL_D(s3, s2, s1, s0) ^ k[3];
+#undef AES_FINAL_D
+    }
+    return o;
+}
+
+// Round key r as an indexable view of the by-value parameter (constant bank).
+struct KeyAt {
+    const RK& rk;
+    int r;
+    __device__ __forceinline__ uint32_t operator[](int j) const { return rk.w[4 * r + j]; }
+};
+
+// One block: Algorithm 1 (corrected, R1) with the Eq 26 round.
+template <int NR, bool DEC, class TB>
+__device__ __forceinline__ uint4 cipher_block(const TB& tb, uint4 v, const RK& rk) {
+    // A6: round-0 AddRoundKey (Eq 21)
+    uint32_t s0 = v.x ^ rk.w[0], s1 = v.y ^ rk.w[1], s2 = v.z ^ rk.w[2], s3 = v.w ^ rk.w[3];
+#pragma unroll
+    for (int r = 1; r < NR; r++) t_round<DEC>(tb, s0, s1, s2, s3, KeyAt{rk, r});   // A7
+    return final_round<DEC>(tb, s0, s1, s2, s3, KeyAt{rk, NR});                    // A8
+}
+
+}  // namespace aesb200

@@ -29,224 +29,12 @@
 
 #include <cstdint>
 #include <cstring>
-#include <mutex>
-#include <vector>
 
 #include "aes_b200.h"
-#include "aes_tables.h"
+#include "aes_device.cuh"
+#include "aes_host.h"
 
 namespace aesb200 {
-
-// ---------------------------------------------------------------------------
-// Table images (compile time) in global and constant memory
-// ---------------------------------------------------------------------------
-struct Tables4 {
-    uint32_t te[4][256];   // Te0..Te3 (Eqs 22-25)
-    uint32_t td[4][256];   // Td0..Td3
-    uint32_t si4[256];     // Si[x] replicated in all four bytes
-};
-
-constexpr uint32_t rotl32(uint32_t v, int n) { return n ? (v << n) | (v >> (32 - n)) : v; }
-
-constexpr Tables4 build_tables4() {
-    Tables4 t{};
-    for (int i = 0; i < 4; i++)
-        for (int x = 0; x < 256; x++) {
-            t.te[i][x] = rotl32(kTables.te0[x], 8 * i);
-            t.td[i][x] = rotl32(kTables.td0[x], 8 * i);
-        }
-    for (int x = 0; x < 256; x++) t.si4[x] = 0x01010101u * kTables.si[x];
-    return t;
-}
-
-constexpr Tables4 kTables4 = build_tables4();
-static_assert(kTables4.te[1][0] == 0x6363C6A5u, "Te1 = rotl(Te0, 8)");
-
-__device__ const Tables4 g_tab = kTables4;     // L2-resident source of the smem fill
-__constant__ Tables4 c_tab = kTables4;         // AES_VAR_CONST (the paper's placement)
-
-struct RK {
-    uint32_t w[60];
-};
-
-constexpr int kThreads = 1024;
-
-// Replicated layout (bytes).  Region C (Si4) is only used by decryption.
-constexpr uint32_t kRegion = 65536;
-__host__ __device__ constexpr uint32_t off_t(int i) { return (uint32_t)(i >> 1) * kRegion + (uint32_t)(i & 1) * 128u; }
-constexpr uint32_t kOffSi = 2 * kRegion;
-constexpr size_t kSmemReplEnc = 2 * kRegion;
-constexpr size_t kSmemReplDec = 2 * kRegion + 255 * 256 + 128;
-constexpr size_t kSmemPlain = (4 * 256 + 256) * 4;
-
-enum { V_REPL = 1, V_PLAIN = 2, V_CONST = 3 };
-
-// ---------------------------------------------------------------------------
-// Table access policies: t(i, s, k) = T_i[byte k of s];  si(s, k) = Si4[byte k of s]
-// ---------------------------------------------------------------------------
-template <int V>
-struct Tab;
-
-template <>
-struct Tab<V_REPL> {
-    const char* sb;
-    uint32_t lo;  // lane*4 in byte 0
-    __device__ __forceinline__ uint32_t t(int i, uint32_t s, int k) const {
-        return *reinterpret_cast<const uint32_t*>(sb + off_t(i) + __byte_perm(lo, s, 0x1140 + 16 * k));
-    }
-    __device__ __forceinline__ uint32_t si(uint32_t s, int k) const {
-        return *reinterpret_cast<const uint32_t*>(sb + kOffSi + __byte_perm(lo, s, 0x1140 + 16 * k));
-    }
-    template <bool DEC>
-    __device__ __forceinline__ static Tab setup(uint32_t* smem) {
-        const uint32_t* src = DEC ? &g_tab.td[0][0] : &g_tab.te[0][0];
-        uint4* s4 = reinterpret_cast<uint4*>(smem);
-        // regions A,B: 32768 words; word w -> x = (w>>6)&255, table i = 2*(w>>14) + ((w>>5)&1)
-        // blockDim.x == kThreads: fixed trip counts, fully unrolled so every
-        // (L2-resident) table load of a thread is in flight at once
-        uint32_t v[8192 / kThreads];
-#pragma unroll
-        for (int it = 0; it < 8192 / kThreads; it++) {
-            int w = 4 * (threadIdx.x + it * kThreads);
-            int x = (w >> 6) & 255, i = 2 * (w >> 14) + ((w >> 5) & 1);
-            v[it] = __ldg(src + i * 256 + x);
-        }
-#pragma unroll
-        for (int it = 0; it < 8192 / kThreads; it++)
-            s4[threadIdx.x + it * kThreads] = make_uint4(v[it], v[it], v[it], v[it]);
-        if (DEC) {
-#pragma unroll
-            for (int it = 0; it < 2048 / kThreads; it++) {
-                int q = threadIdx.x + it * kThreads;
-                int x = q >> 3, part = q & 7;
-                uint32_t u = __ldg(g_tab.si4 + x);
-                s4[(kOffSi + x * 256) / 16 + part] = make_uint4(u, u, u, u);
-            }
-        }
-        __syncthreads();
-        Tab tb;
-        tb.sb = reinterpret_cast<const char*>(smem);
-        tb.lo = (threadIdx.x & 31) * 4;
-        return tb;
-    }
-};
-
-template <>
-struct Tab<V_PLAIN> {
-    const uint32_t* sm;
-    __device__ __forceinline__ uint32_t t(int i, uint32_t s, int k) const {
-        return sm[i * 256 + ((s >> (8 * k)) & 255)];
-    }
-    __device__ __forceinline__ uint32_t si(uint32_t s, int k) const {
-        return sm[1024 + ((s >> (8 * k)) & 255)];
-    }
-    template <bool DEC>
-    __device__ __forceinline__ static Tab setup(uint32_t* smem) {
-        const uint32_t* src = DEC ? &g_tab.td[0][0] : &g_tab.te[0][0];
-        for (int w = threadIdx.x; w < 1024; w += blockDim.x) smem[w] = src[w];
-        for (int w = threadIdx.x; w < 256; w += blockDim.x) smem[1024 + w] = g_tab.si4[w];
-        __syncthreads();
-        Tab tb;
-        tb.sm = smem;
-        return tb;
-    }
-};
-
-template <bool DEC>
-struct ConstSel;
-template <>
-struct ConstSel<false> {
-    __device__ __forceinline__ static uint32_t get(int i, uint32_t x) { return c_tab.te[i][x]; }
-};
-template <>
-struct ConstSel<true> {
-    __device__ __forceinline__ static uint32_t get(int i, uint32_t x) { return c_tab.td[i][x]; }
-};
-
-template <>
-struct Tab<V_CONST> {
-    bool dec;
-    __device__ __forceinline__ uint32_t t(int i, uint32_t s, int k) const {
-        uint32_t x = (s >> (8 * k)) & 255;
-        return dec ? ConstSel<true>::get(i, x) : ConstSel<false>::get(i, x);
-    }
-    __device__ __forceinline__ uint32_t si(uint32_t s, int k) const { return c_tab.si4[(s >> (8 * k)) & 255]; }
-    template <bool DEC>
-    __device__ __forceinline__ static Tab setup(uint32_t*) {
-        Tab tb;
-        tb.dec = DEC;
-        return tb;
-    }
-};
-
-// ---------------------------------------------------------------------------
-// One block: Algorithm 1 (corrected, R1) with the Eq 26 round
-// ---------------------------------------------------------------------------
-// A7: one Eq 26 round on the state (s0..s3) with round key k[0..3].
-// Encryption: e_j = T0[b0(s_j)] ^ T1[b1(s_{j+1})] ^ T2[b2(s_{j+2})] ^ T3[b3(s_{j+3})] ^ k_j.
-// Decryption (equivalent inverse, R12): Td tables with s_j, s_{j-1}, s_{j-2}, s_{j-3}.
-template <bool DEC, class TB, class K>
-__device__ __forceinline__ void t_round(const TB& tb, uint32_t& s0, uint32_t& s1, uint32_t& s2, uint32_t& s3,
-                                        const K& k) {
-    uint32_t e0, e1, e2, e3;
-    if (!DEC) {
-        e0 = tb.t(0, s0, 0) ^ tb.t(1, s1, 1) ^ tb.t(2, s2, 2) ^ tb.t(3, s3, 3) ^ k[0];
-        e1 = tb.t(0, s1, 0) ^ tb.t(1, s2, 1) ^ tb.t(2, s3, 2) ^ tb.t(3, s0, 3) ^ k[1];
-        e2 = tb.t(0, s2, 0) ^ tb.t(1, s3, 1) ^ tb.t(2, s0, 2) ^ tb.t(3, s1, 3) ^ k[2];
-        e3 = tb.t(0, s3, 0) ^ tb.t(1, s0, 1) ^ tb.t(2, s1, 2) ^ tb.t(3, s2, 3) ^ k[3];
-    } else {
-        e0 = tb.t(0, s0, 0) ^ tb.t(1, s3, 1) ^ tb.t(2, s2, 2) ^ tb.t(3, s1, 3) ^ k[0];
-        e1 = tb.t(0, s1, 0) ^ tb.t(1, s0, 1) ^ tb.t(2, s3, 2) ^ tb.t(3, s2, 3) ^ k[1];
-        e2 = tb.t(0, s2, 0) ^ tb.t(1, s1, 1) ^ tb.t(2, s0, 2) ^ tb.t(3, s3, 3) ^ k[2];
-        e3 = tb.t(0, s3, 0) ^ tb.t(1, s2, 1) ^ tb.t(2, s1, 2) ^ tb.t(3, s0, 3) ^ k[3];
-    }
-    s0 = e0; s1 = e1; s2 = e2; s3 = e3;
-}
-
-// A8: final round = SubBytes + ShiftRows + AddRoundKey, no MixColumns (R1, R14).
-template <bool DEC, class TB, class K>
-__device__ __forceinline__ uint4 final_round(const TB& tb, uint32_t s0, uint32_t s1, uint32_t s2, uint32_t s3,
-                                             const K& k) {
-    uint4 o;
-    if (!DEC) {
-        // S[x] sits in byte 0 of Te2, byte 1 of Te3, byte 2 of Te0, byte 3 of Te1
-#define AES_FINAL_E(a, b, c, d) \
-    (((tb.t(2, a, 0) & 0x000000FFu) | (tb.t(3, b, 1) & 0x0000FF00u) | (tb.t(0, c, 2) & 0x00FF0000u) | \
-      (tb.t(1, d, 3) & 0xFF000000u)))
-        o.x = AES_FINAL_E(s0, s1, s2, s3) ^ k[0];
-        o.y = AES_FINAL_E(s1, s2, s3, s0) ^ k[1];
-        o.z = AES_FINAL_E(s2, s3, s0, s1) ^ k[2];
-        o.w = AES_FINAL_E(s3, s0, s1, s2) ^ k[3];
-#undef AES_FINAL_E
-    } else {
-#define AES_FINAL_D(a, b, c, d) \
-    (((tb.si(a, 0) & 0x000000FFu) | (tb.si(b, 1) & 0x0000FF00u) | (tb.si(c, 2) & 0x00FF0000u) | \
-      (tb.si(d, 3) & 0xFF000000u)))
-        o.x = AES_FINAL_D(s0, s3, s2, s1) ^ k[0];
-        o.y = AES_FINAL_D(s1, s0, s3, s2) ^ k[1];
-        o.z = AES_FINAL_D(s2, s1, s0, s3) ^ k[2];
-        o.w = AES_FINAL_D(s3, s2, s1, s0) ^ k[3];
-#undef AES_FINAL_D
-    }
-    return o;
-}
-
-// Round key r as an indexable view of the by-value parameter (constant bank).
-struct KeyAt {
-    const RK& rk;
-    int r;
-    __device__ __forceinline__ uint32_t operator[](int j) const { return rk.w[4 * r + j]; }
-};
-
-// One block: Algorithm 1 (corrected, R1) with the Eq 26 round.
-template <int NR, bool DEC, class TB>
-__device__ __forceinline__ uint4 cipher_block(const TB& tb, uint4 v, const RK& rk) {
-    // A6: round-0 AddRoundKey (Eq 21)
-    uint32_t s0 = v.x ^ rk.w[0], s1 = v.y ^ rk.w[1], s2 = v.z ^ rk.w[2], s3 = v.w ^ rk.w[3];
-#pragma unroll
-    for (int r = 1; r < NR; r++) t_round<DEC>(tb, s0, s1, s2, s3, KeyAt{rk, r});   // A7
-    return final_round<DEC>(tb, s0, s1, s2, s3, KeyAt{rk, NR});                    // A8
-}
 
 // ---------------------------------------------------------------------------
 // Kernels: persistent grid-stride, SPT states per thread per trip.
@@ -324,92 +112,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     aes_body<NR, true, V_REPL, 1, M_CBCD>(in, out, n, rk, mp);
 }
 
-// ---------------------------------------------------------------------------
-// Batched multi-message ECB (aes_ecb_batch): many messages, each with its own
-// key, in ONE launch -- the paper's file-sized workloads at
-// bulk rate instead of one launch per file.  Segment s covers global blocks
-// [first, first + n); a warp's 32 consecutive global blocks find their
-// segment with one warp-uniform binary search (broadcast loads) plus a short
-// forward walk; round keys are read per round from the (L1-resident)
-// descriptor area: a broadcast when the warp is inside one message.
-// ---------------------------------------------------------------------------
-struct BatchSeg {
-    uint64_t in_off, out_off;   // byte offsets from in_base / out_base
-    uint64_t first, n;          // global block range
-    uint32_t key, pad;          // index into the key words (60 per key)
-};
-
-struct KeyVec {
-    uint4 k;   // one round key, fetched with a single LDS.128 (a broadcast within a message)
-    __device__ __forceinline__ uint32_t operator[](int j) const { return j == 0 ? k.x : j == 1 ? k.y : j == 2 ? k.z : k.w; }
-};
-
-constexpr int kBatchMaxKeys = 128;   // 128 x 240 B = 30 KiB of key schedules staged in shared memory
-
-// Each CTA owns one contiguous range of global blocks; its 1024 threads walk it
-// 1024 consecutive blocks per trip, so the segment of a warp only moves
-// forward: found once by a warp-uniform binary search, then advanced by a
-// short forward walk (broadcast loads).
-template <int NR, bool DEC>
-__global__ void __launch_bounds__(kThreads, 1)
-    batch_kernel(const char* __restrict__ in_base, char* __restrict__ out_base, const BatchSeg* __restrict__ segs,
-                 uint32_t nsegs, uint64_t total, const uint32_t* __restrict__ keyw, int nkeys) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    const Tab<V_REPL> tb = Tab<V_REPL>::template setup<DEC>(smem);   // ends with __syncthreads
-    uint32_t* skeys = smem + (DEC ? kSmemReplDec : kSmemReplEnc) / 4;
-    for (int w = threadIdx.x; w < 60 * nkeys; w += blockDim.x) skeys[w] = __ldg(keyw + w);
-    __syncthreads();
-    const uint64_t per = (total + gridDim.x - 1) / gridDim.x;
-    const uint64_t c0 = per * blockIdx.x, c1 = c0 + per < total ? c0 + per : total;
-    const uint32_t lane = threadIdx.x & 31;
-    uint64_t w0 = c0 + (threadIdx.x & ~31u);   // warp-uniform start of this warp's 32 blocks
-    if (w0 >= c1) return;                       // (no barriers below)
-    uint32_t seg;
-    {   // last segment with first <= w0: warp-uniform binary search (broadcast loads)
-        uint32_t lo = 0, hi = nsegs - 1;
-        while (lo < hi) {
-            uint32_t mid = (lo + hi + 1) >> 1;
-            if (__ldg(&segs[mid].first) <= w0) lo = mid; else hi = mid - 1;
-        }
-        seg = lo;
-    }
-    // Software pipeline: the segment walk and the 128-bit load of the NEXT trip
-    // are issued before the rounds of the current one, hiding their latency chain.
-    bool have = false;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    uint4* op = nullptr;
-    const uint4* kp = nullptr;
-    auto fetch = [&](uint64_t base) {
-        while (base >= __ldg(&segs[seg].first) + __ldg(&segs[seg].n)) seg++;   // warp-uniform advance
-        const uint64_t i = base + lane;
-        have = i < c1;
-        if (!have) return;
-        uint32_t sidx = seg;
-        while (i >= __ldg(&segs[sidx].first) + __ldg(&segs[sidx].n)) sidx++;
-        const BatchSeg* sg = segs + sidx;
-        const uint64_t local = i - __ldg(&sg->first);
-        v = __ldcs(reinterpret_cast<const uint4*>(in_base + __ldg(&sg->in_off)) + local);
-        op = reinterpret_cast<uint4*>(out_base + __ldg(&sg->out_off)) + local;
-        kp = reinterpret_cast<const uint4*>(skeys + 60u * __ldg(&sg->key));
-    };
-    fetch(w0);
-    while (w0 < c1) {
-        const bool chave = have;
-        const uint4 cv = v;
-        uint4* const cop = op;
-        const uint4* const ckp = kp;
-        w0 += blockDim.x;
-        if (w0 < c1) fetch(w0);
-        if (chave) {
-            const uint4 k0 = ckp[0];
-            uint32_t s0 = cv.x ^ k0.x, s1 = cv.y ^ k0.y, s2 = cv.z ^ k0.z, s3 = cv.w ^ k0.w;
-#pragma unroll
-            for (int r = 1; r < NR; r++) t_round<DEC>(tb, s0, s1, s2, s3, KeyVec{ckp[r]});
-            __stcs(cop, final_round<DEC>(tb, s0, s1, s2, s3, KeyVec{ckp[NR]}));
-        }
-    }
-}
-
 // Debug/pin kernel (aes_ecb_trace): the state after ARK(0) and `rounds` rounds
 // of the SAME t_round / final_round code the production kernels inline, one
 // state per thread.  rounds = NR gives the full cipher.
@@ -457,12 +159,8 @@ __global__ void __launch_bounds__(kThreads, 1) lds_gather_kernel(uint32_t* sink,
 }
 
 // ---------------------------------------------------------------------------
-// Host side: kernel registry, per-device attribute cache, validation, launch
+// Host side: kernel registry and launch
 // ---------------------------------------------------------------------------
-struct KernelInfo {
-    const void* fn;
-    size_t smem;
-};
 
 template <int NR, bool DEC, int V, int SPT>
 KernelInfo kinfo() {
@@ -504,106 +202,6 @@ KernelInfo pick_mode(int nr, int mode) {
     f = nr == 10 ? (const void*)&cbc_decrypt_kernel<10> : nr == 12 ? (const void*)&cbc_decrypt_kernel<12>
                                                                    : (const void*)&cbc_decrypt_kernel<14>;
     return {f, kSmemReplDec};
-}
-
-thread_local int t_last_cuda_error = 0;
-
-inline aes_status cuda_fail(cudaError_t e) {
-    t_last_cuda_error = (int)e;
-    return AES_ECUDA;
-}
-
-// Per-(device, kernel) resident-CTA count; set the dynamic-smem attribute once.
-constexpr int kMaxDev = 64;
-std::mutex g_attr_mu;
-struct AttrEntry {
-    const void* fn;
-    int occ;
-};
-AttrEntry g_attr[kMaxDev][128];
-int g_nsm[kMaxDev];
-
-aes_status resident_ctas(int dev, const KernelInfo& ki, int* occ, int* nsm) {
-    if (dev < 0 || dev >= kMaxDev) return AES_ERANGE;
-    std::lock_guard<std::mutex> g(g_attr_mu);
-    if (!g_nsm[dev]) {
-        int v = 0;
-        cudaError_t e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        if (e != cudaSuccess) return cuda_fail(e);
-        g_nsm[dev] = v;
-    }
-    *nsm = g_nsm[dev];
-    int slot = -1;
-    for (int s = 0; s < 128; s++) {
-        if (g_attr[dev][s].fn == ki.fn) { *occ = g_attr[dev][s].occ; return AES_OK; }
-        if (!g_attr[dev][s].fn) { slot = s; break; }
-    }
-    if (slot < 0) return AES_ERANGE;
-    cudaError_t e = cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ki.smem);
-    if (e != cudaSuccess) return cuda_fail(e);
-    int o = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ki.fn, kThreads, ki.smem);
-    if (e != cudaSuccess) return cuda_fail(e);
-    if (o < 1) o = 1;
-    g_attr[dev][slot].fn = ki.fn;
-    g_attr[dev][slot].occ = o;
-    *occ = o;
-    return AES_OK;
-}
-
-// A library-owned stream-ordered memory pool per device for small per-call
-// descriptors (aes_ecb_batch): memory stays cached between calls (a release
-// threshold of 64 MiB) instead of being unmapped at every synchronisation as
-// with the default pool's threshold of 0; torch's allocator is not touched.
-std::mutex g_pool_mu;
-cudaMemPool_t g_pool[kMaxDev];
-
-aes_status desc_pool(int dev, cudaMemPool_t* out) {
-    if (dev < 0 || dev >= kMaxDev) return AES_ERANGE;
-    std::lock_guard<std::mutex> g(g_pool_mu);
-    if (!g_pool[dev]) {
-        cudaMemPoolProps props = {};
-        props.allocType = cudaMemAllocationTypePinned;
-        props.location.type = cudaMemLocationTypeDevice;
-        props.location.id = dev;
-        cudaMemPool_t p;
-        cudaError_t e = cudaMemPoolCreate(&p, &props);
-        if (e != cudaSuccess) return cuda_fail(e);
-        uint64_t keep = 64ull << 20;
-        cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
-        g_pool[dev] = p;
-    }
-    *out = g_pool[dev];
-    return AES_OK;
-}
-
-aes_status validate_keys(const aes_round_keys* rk, int nr) {
-    if (!rk) return AES_ENULL;
-    if ((nr != 10 && nr != 12 && nr != 14) || rk->nr != nr || rk->keybits != 32 * (nr - 6)) return AES_ENR;
-    return AES_OK;
-}
-
-aes_status validate_buffers(const void* in, const void* out, uint64_t nblocks) {
-    if (!in || !out) return AES_ENULL;
-    if (nblocks > (UINT64_MAX >> 4)) return AES_ERANGE;
-    uint64_t bytes = nblocks << 4;
-    uintptr_t a = (uintptr_t)in, b = (uintptr_t)out;
-    if ((a | b) & 15) return AES_EALIGN;
-    if (a > UINTPTR_MAX - bytes || b > UINTPTR_MAX - bytes) return AES_ERANGE;
-    if (a != b && a < b + bytes && b < a + bytes) return AES_EOVERLAP;
-    return AES_OK;
-}
-
-aes_status check_device_ptr(const void* p, int dev) {
-    cudaPointerAttributes at;
-    cudaError_t e = cudaPointerGetAttributes(&at, p);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        return cuda_fail(e);
-    }
-    if ((at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) || at.device != dev)
-        return AES_ENOTDEVICE;
-    return AES_OK;
 }
 
 aes_status launch(const aes_round_keys* rk, int nr, int decrypt, const void* in, void* out, uint64_t nblocks,
@@ -648,6 +246,11 @@ aes_status launch(const aes_round_keys* rk, int nr, int decrypt, const void* in,
     e = cudaLaunchKernel(ki.fn, dim3(grid), dim3(kThreads), args, ki.smem, stream);
     if (e != cudaSuccess) return cuda_fail(e);
     return AES_OK;
+}
+
+aes_status launch_ecb(const aes_round_keys* rk, int nr, int decrypt, const void* in, void* out, uint64_t nblocks,
+                      cudaStream_t stream, bool check_ptrs) {
+    return launch(rk, nr, decrypt, in, out, nblocks, stream, nullptr, check_ptrs);
 }
 
 }  // namespace aesb200
@@ -727,76 +330,6 @@ aes_status aes_ecb_trace(const aes_round_keys* rk, int nr, int decrypt, int roun
     return e == cudaSuccess ? AES_OK : cuda_fail(e);
 }
 
-aes_status aes_ecb_batch(const aes_round_keys* keys, int nkeys, int decrypt, const aes_segment* segs, uint32_t nsegs,
-                         const void* in_base, void* out_base, void* stream) {
-    if (!keys) return AES_ENULL;
-    if (nkeys < 1 || nkeys > kBatchMaxKeys) return AES_ERANGE;
-    const int nr = keys[0].nr;
-    for (int k = 0; k < nkeys; k++) {
-        aes_status st = validate_keys(&keys[k], nr);
-        if (st) return st;
-    }
-    if (nsegs == 0) return AES_OK;
-    if (!segs || !in_base || !out_base) return AES_ENULL;
-    if (((uintptr_t)in_base | (uintptr_t)out_base) & 15) return AES_EALIGN;
-    std::vector<BatchSeg> hs(nsegs);
-    uint64_t total = 0;
-    for (uint32_t i = 0; i < nsegs; i++) {
-        const aes_segment& a = segs[i];
-        if (a.key_index >= (uint32_t)nkeys) return AES_ERANGE;
-        if ((a.in_offset | a.out_offset) & 15) return AES_EALIGN;
-        if (a.nblocks > (UINT64_MAX >> 4) || total + a.nblocks < total) return AES_ERANGE;
-        uint64_t bytes = a.nblocks << 4;
-        uintptr_t pi = (uintptr_t)in_base + a.in_offset, po = (uintptr_t)out_base + a.out_offset;
-        if (pi < (uintptr_t)in_base || po < (uintptr_t)out_base || pi > UINTPTR_MAX - bytes || po > UINTPTR_MAX - bytes)
-            return AES_ERANGE;
-        if (pi != po && pi < po + bytes && po < pi + bytes) return AES_EOVERLAP;
-        hs[i] = BatchSeg{a.in_offset, a.out_offset, total, a.nblocks, a.key_index, 0};
-        total += a.nblocks;
-    }
-    if (total == 0) return AES_OK;
-    int dev = 0, occ = 1, nsm = 148;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return cuda_fail(e);
-    aes_status st;
-    if ((st = check_device_ptr(in_base, dev))) return st;
-    if (out_base != in_base && (st = check_device_ptr(out_base, dev))) return st;
-    const void* f = nullptr;
-    if (nr == 10) f = decrypt ? (const void*)&batch_kernel<10, true> : (const void*)&batch_kernel<10, false>;
-    else if (nr == 12) f = decrypt ? (const void*)&batch_kernel<12, true> : (const void*)&batch_kernel<12, false>;
-    else f = decrypt ? (const void*)&batch_kernel<14, true> : (const void*)&batch_kernel<14, false>;
-    KernelInfo ki{f, (decrypt ? kSmemReplDec : kSmemReplEnc) + 240 * kBatchMaxKeys};
-    if ((st = resident_ctas(dev, ki, &occ, &nsm))) return st;
-    const size_t smem = (decrypt ? kSmemReplDec : kSmemReplEnc) + 240ull * nkeys;
-    // descriptors: segments, then 60 key words per key (ek or dk), in one
-    // stream-ordered allocation that is freed after the kernel on `stream`
-    const size_t seg_bytes = sizeof(BatchSeg) * nsegs, key_bytes = 240ull * nkeys;
-    std::vector<char> host(seg_bytes + key_bytes);
-    std::memcpy(host.data(), hs.data(), seg_bytes);
-    for (int k = 0; k < nkeys; k++)
-        std::memcpy(host.data() + seg_bytes + 240ull * k, decrypt ? keys[k].dk : keys[k].ek, 240);
-    cudaStream_t cs = (cudaStream_t)stream;
-    cudaMemPool_t pool;
-    if ((st = desc_pool(dev, &pool))) return st;
-    void* d = nullptr;
-    if ((e = cudaMallocFromPoolAsync(&d, host.size(), pool, cs)) != cudaSuccess) return cuda_fail(e);
-    if ((e = cudaMemcpyAsync(d, host.data(), host.size(), cudaMemcpyHostToDevice, cs)) != cudaSuccess) {
-        cudaFreeAsync(d, cs);
-        return cuda_fail(e);
-    }
-    const char* pin = static_cast<const char*>(in_base);
-    char* pout = static_cast<char*>(out_base);
-    const BatchSeg* dsegs = static_cast<const BatchSeg*>(d);
-    const uint32_t* dkeys = reinterpret_cast<const uint32_t*>(static_cast<char*>(d) + seg_bytes);
-    void* args[] = {(void*)&pin, (void*)&pout, (void*)&dsegs, (void*)&nsegs, (void*)&total, (void*)&dkeys,
-                    (void*)&nkeys};
-    uint64_t want = (total + 31) / 32, cap = (uint64_t)nsm * occ;
-    e = cudaLaunchKernel(f, dim3((unsigned)(want < cap ? want : cap)), dim3(kThreads), args, smem, cs);
-    cudaError_t e2 = cudaFreeAsync(d, cs);
-    if (e != cudaSuccess) return cuda_fail(e);
-    return e2 == cudaSuccess ? AES_OK : cuda_fail(e2);
-}
-
 aes_status aes_mb_lds_gather(void* sink, int grid, int iters, void* stream) {
     if (!sink) return AES_ENULL;
     if (grid <= 0 || iters < 0) return AES_ERANGE;
@@ -810,108 +343,5 @@ aes_status aes_mb_lds_gather(void* sink, int grid, int iters, void* stream) {
     e = cudaGetLastError();
     return e == cudaSuccess ? AES_OK : cuda_fail(e);
 }
-
-// --------------------------------------------------------------------------
-// Host-resident pipeline (NEXT-3)
-// --------------------------------------------------------------------------
-struct aes_pipeline {
-    int device;
-    uint64_t chunk;
-    int depth;
-    void* dbuf[8];
-    cudaStream_t st[8];
-};
-
-aes_status aes_pipeline_destroy(aes_pipeline* p) {
-    if (!p) return AES_ENULL;
-    int prev = 0;
-    cudaGetDevice(&prev);
-    cudaSetDevice(p->device);
-    for (int k = 0; k < p->depth; k++) {
-        if (p->st[k]) cudaStreamSynchronize(p->st[k]), cudaStreamDestroy(p->st[k]);
-        if (p->dbuf[k]) cudaFree(p->dbuf[k]);
-    }
-    cudaSetDevice(prev);
-    delete p;
-    return AES_OK;
-}
-
-aes_status aes_pipeline_create(uint64_t chunk_bytes, int depth, aes_pipeline** out) {
-    if (!out) return AES_ENULL;
-    *out = nullptr;
-    if (chunk_bytes < 16 || (chunk_bytes & 15) || depth < 1 || depth > 8) return AES_ERANGE;
-    aes_pipeline* p = new aes_pipeline();
-    p->chunk = chunk_bytes;
-    p->depth = depth;
-    cudaError_t e = cudaGetDevice(&p->device);
-    if (e != cudaSuccess) { delete p; return cuda_fail(e); }
-    for (int k = 0; k < depth; k++) {
-        e = cudaMalloc(&p->dbuf[k], chunk_bytes);
-        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->st[k], cudaStreamNonBlocking);
-        if (e != cudaSuccess) {
-            aes_pipeline_destroy(p);
-            return cuda_fail(e);
-        }
-    }
-    *out = p;
-    return AES_OK;
-}
-
-aes_status aes_pipeline_run(aes_pipeline* p, const aes_round_keys* rk, int nr, int decrypt, const void* in_host,
-                            void* out_host, uint64_t nblocks) {
-    if (!p) return AES_ENULL;
-    aes_status st = validate_keys(rk, nr);
-    if (st) return st;
-    if (nblocks == 0) return AES_OK;
-    if (!in_host || !out_host) return AES_ENULL;
-    if (nblocks > (UINT64_MAX >> 4)) return AES_ERANGE;
-    uint64_t bytes = nblocks << 4;
-    uintptr_t a = (uintptr_t)in_host, b = (uintptr_t)out_host;
-    if (a > UINTPTR_MAX - bytes || b > UINTPTR_MAX - bytes) return AES_ERANGE;
-    if (a != b && a < b + bytes && b < a + bytes) return AES_EOVERLAP;
-    int prev = 0;
-    cudaError_t e = cudaGetDevice(&prev);
-    if (e != cudaSuccess) return cuda_fail(e);
-    if (prev != p->device && (e = cudaSetDevice(p->device)) != cudaSuccess) return cuda_fail(e);
-    const char* src = static_cast<const char*>(in_host);
-    char* dst = static_cast<char*>(out_host);
-    uint64_t nchunks = (bytes + p->chunk - 1) / p->chunk;
-    for (uint64_t c = 0; c < nchunks && st == AES_OK; c++) {
-        int k = (int)(c % (uint64_t)p->depth);
-        uint64_t off = c * p->chunk;
-        uint64_t len = bytes - off < p->chunk ? bytes - off : p->chunk;
-        e = cudaMemcpyAsync(p->dbuf[k], src + off, len, cudaMemcpyHostToDevice, p->st[k]);
-        if (e != cudaSuccess) { st = cuda_fail(e); break; }
-        st = launch(rk, nr, decrypt, p->dbuf[k], p->dbuf[k], len >> 4, p->st[k], nullptr, false);
-        if (st) break;
-        e = cudaMemcpyAsync(dst + off, p->dbuf[k], len, cudaMemcpyDeviceToHost, p->st[k]);
-        if (e != cudaSuccess) { st = cuda_fail(e); break; }
-    }
-    for (int k = 0; k < p->depth; k++) {
-        e = cudaStreamSynchronize(p->st[k]);
-        if (e != cudaSuccess && st == AES_OK) st = cuda_fail(e);
-    }
-    if (prev != p->device) cudaSetDevice(prev);
-    return st;
-}
-
-const char* aes_status_string(aes_status s) {
-    switch (s) {
-        case AES_OK: return "AES_OK";
-        case AES_EKEYBITS: return "AES_EKEYBITS: keybits must be 128, 192 or 256";
-        case AES_ENR: return "AES_ENR: nr must be 10/12/14 and match the round keys";
-        case AES_ENULL: return "AES_ENULL: required pointer is NULL";
-        case AES_EALIGN: return "AES_EALIGN: buffers must be 16-byte aligned";
-        case AES_EOVERLAP: return "AES_EOVERLAP: in and out partially overlap";
-        case AES_ERANGE: return "AES_ERANGE: size or configuration out of range";
-        case AES_ENOTDEVICE: return "AES_ENOTDEVICE: buffer is not device memory of the current device";
-        case AES_ECUDA: return "AES_ECUDA: CUDA runtime error (see aes_last_cuda_error)";
-        case AES_EVARIANT: return "AES_EVARIANT: unknown kernel variant or states_per_thread";
-    }
-    return "AES_?: unknown status";
-}
-
-int aes_last_cuda_error(void) { return t_last_cuda_error; }
-int aes_abi_version(void) { return AES_B200_ABI_VERSION; }
 
 }  // extern "C"

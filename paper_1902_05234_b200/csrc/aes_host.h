@@ -1,0 +1,32 @@
+// aes_host.h -- host-side helpers shared by the TUs of libaes_b200.so:
+// kernel registry entries, per-device attribute cache, descriptor pool,
+// argument validation, CUDA error capture.  Defined in aes_runtime.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "aes_b200.h"
+
+namespace aesb200 {
+
+struct KernelInfo {
+    const void* fn;
+    size_t smem;
+};
+
+constexpr int kMaxDev = 64;
+constexpr int kThreads = 1024;   // every kernel runs 1024-thread CTAs (one per SM)
+
+aes_status cuda_fail(cudaError_t e);                       // records e for aes_last_cuda_error()
+aes_status resident_ctas(int dev, const KernelInfo& ki, int* occ, int* nsm);   // sets smem attr once
+aes_status desc_pool(int dev, cudaMemPool_t* out);         // stream-ordered pool for descriptors
+aes_status validate_keys(const aes_round_keys* rk, int nr);
+aes_status validate_buffers(const void* in, const void* out, uint64_t nblocks);
+aes_status check_device_ptr(const void* p, int dev);
+// ECB launch used by the host pipeline (aes_ecb.cu)
+aes_status launch_ecb(const aes_round_keys* rk, int nr, int decrypt, const void* in, void* out, uint64_t nblocks,
+                      cudaStream_t stream, bool check_ptrs);
+
+}  // namespace aesb200

@@ -1,0 +1,138 @@
+// aes_runtime.cu -- host runtime of libaes_b200.so: CUDA error capture,
+// the per-device launch-attribute cache, the descriptor memory pool, argument
+// validation (everything decided before a launch, include/aes_b200.h "Errors"),
+// status strings.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+
+#include "aes_b200.h"
+#include "aes_host.h"
+
+namespace aesb200 {
+
+thread_local int t_last_cuda_error = 0;
+
+aes_status cuda_fail(cudaError_t e) {
+    t_last_cuda_error = (int)e;
+    return AES_ECUDA;
+}
+
+// Per-(device, kernel) resident-CTA count; set the dynamic-smem attribute once.
+std::mutex g_attr_mu;
+struct AttrEntry {
+    const void* fn;
+    int occ;
+};
+AttrEntry g_attr[kMaxDev][128];
+int g_nsm[kMaxDev];
+
+aes_status resident_ctas(int dev, const KernelInfo& ki, int* occ, int* nsm) {
+    if (dev < 0 || dev >= kMaxDev) return AES_ERANGE;
+    std::lock_guard<std::mutex> g(g_attr_mu);
+    if (!g_nsm[dev]) {
+        int v = 0;
+        cudaError_t e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return cuda_fail(e);
+        g_nsm[dev] = v;
+    }
+    *nsm = g_nsm[dev];
+    int slot = -1;
+    for (int s = 0; s < 128; s++) {
+        if (g_attr[dev][s].fn == ki.fn) { *occ = g_attr[dev][s].occ; return AES_OK; }
+        if (!g_attr[dev][s].fn) { slot = s; break; }
+    }
+    if (slot < 0) return AES_ERANGE;
+    cudaError_t e = cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ki.smem);
+    if (e != cudaSuccess) return cuda_fail(e);
+    int o = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ki.fn, kThreads, ki.smem);
+    if (e != cudaSuccess) return cuda_fail(e);
+    if (o < 1) o = 1;
+    g_attr[dev][slot].fn = ki.fn;
+    g_attr[dev][slot].occ = o;
+    *occ = o;
+    return AES_OK;
+}
+
+// A library-owned stream-ordered memory pool per device for small per-call
+// descriptors (aes_ecb_batch): memory stays cached between calls (a release
+// threshold of 64 MiB) instead of being unmapped at every synchronisation as
+// with the default pool's threshold of 0; torch's allocator is not touched.
+std::mutex g_pool_mu;
+cudaMemPool_t g_pool[kMaxDev];
+
+aes_status desc_pool(int dev, cudaMemPool_t* out) {
+    if (dev < 0 || dev >= kMaxDev) return AES_ERANGE;
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    if (!g_pool[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t p;
+        cudaError_t e = cudaMemPoolCreate(&p, &props);
+        if (e != cudaSuccess) return cuda_fail(e);
+        uint64_t keep = 64ull << 20;
+        cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+        g_pool[dev] = p;
+    }
+    *out = g_pool[dev];
+    return AES_OK;
+}
+
+aes_status validate_keys(const aes_round_keys* rk, int nr) {
+    if (!rk) return AES_ENULL;
+    if ((nr != 10 && nr != 12 && nr != 14) || rk->nr != nr || rk->keybits != 32 * (nr - 6)) return AES_ENR;
+    return AES_OK;
+}
+
+aes_status validate_buffers(const void* in, const void* out, uint64_t nblocks) {
+    if (!in || !out) return AES_ENULL;
+    if (nblocks > (UINT64_MAX >> 4)) return AES_ERANGE;
+    uint64_t bytes = nblocks << 4;
+    uintptr_t a = (uintptr_t)in, b = (uintptr_t)out;
+    if ((a | b) & 15) return AES_EALIGN;
+    if (a > UINTPTR_MAX - bytes || b > UINTPTR_MAX - bytes) return AES_ERANGE;
+    if (a != b && a < b + bytes && b < a + bytes) return AES_EOVERLAP;
+    return AES_OK;
+}
+
+aes_status check_device_ptr(const void* p, int dev) {
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return cuda_fail(e);
+    }
+    if ((at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) || at.device != dev)
+        return AES_ENOTDEVICE;
+    return AES_OK;
+}
+
+}  // namespace aesb200
+
+extern "C" {
+
+const char* aes_status_string(aes_status s) {
+    switch (s) {
+        case AES_OK: return "AES_OK";
+        case AES_EKEYBITS: return "AES_EKEYBITS: keybits must be 128, 192 or 256";
+        case AES_ENR: return "AES_ENR: nr must be 10/12/14 and match the round keys";
+        case AES_ENULL: return "AES_ENULL: required pointer is NULL";
+        case AES_EALIGN: return "AES_EALIGN: buffers must be 16-byte aligned";
+        case AES_EOVERLAP: return "AES_EOVERLAP: in and out partially overlap";
+        case AES_ERANGE: return "AES_ERANGE: size or configuration out of range";
+        case AES_ENOTDEVICE: return "AES_ENOTDEVICE: buffer is not device memory of the current device";
+        case AES_ECUDA: return "AES_ECUDA: CUDA runtime error (see aes_last_cuda_error)";
+        case AES_EVARIANT: return "AES_EVARIANT: unknown kernel variant or states_per_thread";
+    }
+    return "AES_?: unknown status";
+}
+
+int aes_last_cuda_error(void) { return aesb200::t_last_cuda_error; }
+int aes_abi_version(void) { return AES_B200_ABI_VERSION; }
+
+}  // extern "C"
+
