@@ -293,16 +293,24 @@ def run_ours(a):
     lds_peak = looks / (e0.elapsed_time(e1) * 1e-3)          # lookups / s
 
     # ---- step ------------------------------------------------------------
+    nvtx = torch.cuda.nvtx
+
     def step(ev=None):
+        nvtx.range_push("aes step")
         r = aes.expand_key(key)                               # A1/A2 (host)
         if ev:
             ev[0].record(s)
+        nvtx.range_push("aes_ecb_encrypt")
         aes.ecb_encrypt(r, x, out=ct)
+        nvtx.range_pop()
         if ev:
             ev[1].record(s)
+        nvtx.range_push("aes_ecb_decrypt")
         aes.ecb_decrypt(r, ct, out=pt)
+        nvtx.range_pop()
         if ev:
             ev[2].record(s)
+        nvtx.range_pop()
 
     with torch.cuda.stream(s):
         for _ in range(a.warmup):

@@ -407,3 +407,24 @@ def test_batch_thousand_small_files_one_launch(aes):
     outs = aes.ecb_batch([rk], xs, key_index=[0] * 1000)
     got = torch.cat(outs).cpu().numpy()
     assert np.array_equal(got, oracle.encrypt(key, synth.blocks(0, 1000 * n), nthreads=8))
+
+
+def test_pipeline_pageable_numpy_and_errors(aes):
+    """aes_pipeline_run with pageable numpy buffers (no overlap, still correct),
+    chunk sizes that do not divide the message, and its argument errors."""
+    key = synth.key(192)
+    rk = aes.expand_key(key)
+    n = 12345
+    host = synth.blocks(3, n)
+    dst = np.empty_like(host)
+    p = aes.Pipeline(chunk_bytes=16 * 1000, depth=2)
+    p.run(rk, host, dst)
+    assert np.array_equal(dst, oracle.encrypt(key, host, nthreads=8))
+    back = np.empty_like(host)
+    p.run(rk, dst, back, decrypt=True)
+    assert np.array_equal(back, host)
+    with pytest.raises(aes.AesError):
+        p.run(rk, host[:-16 * 5], host[16:-16 * 4])       # partial overlap
+    with pytest.raises(ValueError):
+        p.run(rk, host, dst[:-16])
+    p.close()
