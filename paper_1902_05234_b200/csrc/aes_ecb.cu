@@ -67,18 +67,13 @@ __device__ __forceinline__ void aes_body(const uint4* __restrict__ in, uint4* __
                                          const RK& rk, const ModeP& mp) {
     extern __shared__ __align__(16) uint32_t smem[];
     const Tab<V> tb = Tab<V>::template setup<DEC>(smem);   // A4
-    // Balanced contiguous range per CTA (sizes differ by at most one block),
-    // walked 1024 consecutive blocks per trip: every warp access is 512
-    // contiguous bytes and no CTA carries a partial extra trip.
-    const uint64_t per = n / gridDim.x, rem = n % gridDim.x, b = blockIdx.x;
-    const uint64_t c0 = b * per + (b < rem ? b : rem), c1 = c0 + per + (b < rem ? 1 : 0);
-    const uint64_t T = blockDim.x;
-    for (uint64_t i = c0 + threadIdx.x; i < c1; i += SPT * T) {
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += SPT * T) {
         uint4 v[SPT], w[SPT];
 #pragma unroll
         for (int k = 0; k < SPT; k++) {
             const uint64_t j = i + k * T;
-            if (j < c1) {                                                  // A5
+            if (j < n) {                                                   // A5
                 if (MODE == M_ECB) v[k] = __ldcs(in + j);
                 if (MODE == M_CTR) { v[k] = counter_block(mp, j); w[k] = __ldcs(in + j); }
                 if (MODE == M_CBCD) {
@@ -92,7 +87,7 @@ __device__ __forceinline__ void aes_body(const uint4* __restrict__ in, uint4* __
 #pragma unroll
         for (int k = 0; k < SPT; k++) {
             const uint64_t j = i + k * T;
-            if (j < c1) __stcs(out + j, MODE == M_ECB ? v[k] : xor4(v[k], w[k]));  // A9
+            if (j < n) __stcs(out + j, MODE == M_ECB ? v[k] : xor4(v[k], w[k]));   // A9
         }
     }
 }
