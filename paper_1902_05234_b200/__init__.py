@@ -333,3 +333,16 @@ def lds_gather(sink, grid: int, iters: int, stream=None):
         _check(_native.lib.aes_mb_lds_gather(ctypes.c_void_p(sink.data_ptr()), grid, iters,
                                              ctypes.c_void_p(s.cuda_stream)), "aes_mb_lds_gather")
     return 16 * iters * grid * 1024  # lookups issued
+
+
+# The C ABI's own names (include/aes_b200.h), for callers who mirror the C API.
+aes_expand_key = expand_key
+aes_ecb_encrypt = ecb_encrypt
+aes_ecb_decrypt = ecb_decrypt
+aes_ctr_xcrypt = ctr_xcrypt
+aes_cbc_decrypt = cbc_decrypt
+aes_ecb_batch = ecb_batch
+aes_ecb_trace = ecb_trace
+aes_mb_lds_gather = lds_gather
+__all__ += ["aes_expand_key", "aes_ecb_encrypt", "aes_ecb_decrypt", "aes_ctr_xcrypt", "aes_cbc_decrypt",
+            "aes_ecb_batch", "aes_ecb_trace", "aes_mb_lds_gather"]

@@ -207,3 +207,11 @@ def test_batch_validation():
     ovl = (_native.aes_segment * 1)(_native.aes_segment(0, 16, 4, 0, 0))
     assert L.aes_ecb_batch(keys, 2, 0, ovl, 1, A, A, None) == _native.AES_EOVERLAP
     assert L.aes_ecb_batch(keys, 2, 0, seg, 2, A + 8, A, None) == _native.AES_EALIGN
+
+
+def test_python_binding_mirrors_abi_names():
+    import paper_1902_05234_b200 as aes
+    for name in ("aes_expand_key", "aes_ecb_encrypt", "aes_ecb_decrypt", "aes_ctr_xcrypt", "aes_cbc_decrypt",
+                 "aes_ecb_batch", "aes_ecb_trace", "aes_mb_lds_gather"):
+        assert callable(getattr(aes, name)), name
+    assert aes.aes_expand_key(bytes(16)).ek[:4] == [0, 0, 0, 0]
