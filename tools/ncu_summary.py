@@ -121,7 +121,6 @@ def main():
         md.append("| top warp stall reasons (warps per issue) | " + " | ".join(
             ", ".join(f"{n} {v:.2f}" for n, v in list(k["stalls_per_issue"].items())[:4]) for k in ks) + " |")
         md.append("")
-        shutil.copy(a.rep, os.path.join(prof, f"{a.tag}_full.ncu-rep")) if os.path.getsize(a.rep) < 8 << 20 else None
     if a.launches:
         agg = read_launches(a.launches)
         tot = sum(t for _, t in agg.values())
