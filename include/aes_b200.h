@@ -121,7 +121,7 @@ aes_status aes_cbc_decrypt(const aes_round_keys *rk, int nr, const uint8_t *iv, 
  * leave launch-bound).  Message i = segs[i]: nblocks 16-byte blocks read at
  * in_base + in_offset and written at out_base + out_offset with round keys
  * keys[key_index] (ek, or dk when decrypt = 1).
- *  keys  : host array of 1..128 round keys (staged in shared memory), all
+ *  keys  : host array of 1..128 round keys (passed by value in the kernel parameters), all
  *          with the same nr (else AES_ENR).
  *  segs  : host array of nsegs descriptors; read during the call only (they are
  *          staged to the device in a stream-ordered allocation freed after the

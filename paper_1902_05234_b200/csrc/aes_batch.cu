@@ -18,8 +18,10 @@ namespace aesb200 {
 // bulk rate instead of one launch per file.  Segment s covers global blocks
 // [first, first + n); a warp's 32 consecutive global blocks find their
 // segment with one warp-uniform binary search (broadcast loads) plus a short
-// forward walk; round keys are read per round from the (L1-resident)
-// descriptor area: a broadcast when the warp is inside one message.
+// forward walk.  The key schedules travel BY VALUE in the kernel parameters
+// (constant bank, up to 128 x 240 B): per round a message's round key is an
+// LDC broadcast through the constant cache -- no shared-memory/L1TEX
+// traffic, which is the resource the T-table rounds saturate.
 // ---------------------------------------------------------------------------
 struct BatchSeg {
     uint64_t in_off, out_off;   // byte offsets from in_base / out_base
@@ -27,26 +29,30 @@ struct BatchSeg {
     uint32_t key, pad;          // index into the key words (60 per key)
 };
 
-struct KeyVec {
-    uint4 k;   // one round key, fetched with a single LDS.128 (a broadcast within a message)
-    __device__ __forceinline__ uint32_t operator[](int j) const { return j == 0 ? k.x : j == 1 ? k.y : j == 2 ? k.z : k.w; }
+template <int KCAP>
+struct BatchKeys {
+    uint32_t w[KCAP * 60];   // ek (or dk) of key k at w[60k .. 60k + 4(NR+1))
 };
 
-constexpr int kBatchMaxKeys = 128;   // 128 x 240 B = 30 KiB of key schedules staged in shared memory
+constexpr int kBatchMaxKeys = 128;   // 128 x 240 B = 30 KiB of kernel parameters (limit 32,764 B)
+
+template <int KCAP>
+struct KeyParamAt {
+    const BatchKeys<KCAP>& ks;
+    uint32_t base;   // 60 * key + 4 * round
+    __device__ __forceinline__ uint32_t operator[](int j) const { return ks.w[base + j]; }
+};
 
 // Each CTA owns one contiguous range of global blocks; its 1024 threads walk it
 // 1024 consecutive blocks per trip, so the segment of a warp only moves
 // forward: found once by a warp-uniform binary search, then advanced by a
 // short forward walk (broadcast loads).
-template <int NR, bool DEC>
+template <int NR, bool DEC, int KCAP>
 __global__ void __launch_bounds__(kThreads, 1)
     batch_kernel(const char* __restrict__ in_base, char* __restrict__ out_base, const BatchSeg* __restrict__ segs,
-                 uint32_t nsegs, uint64_t total, const uint32_t* __restrict__ keyw, int nkeys) {
+                 uint32_t nsegs, uint64_t total, const __grid_constant__ BatchKeys<KCAP> keys) {
     extern __shared__ __align__(16) uint32_t smem[];
     const Tab<V_REPL> tb = Tab<V_REPL>::template setup<DEC>(smem);   // ends with __syncthreads
-    uint32_t* skeys = smem + (DEC ? kSmemReplDec : kSmemReplEnc) / 4;
-    for (int w = threadIdx.x; w < 60 * nkeys; w += blockDim.x) skeys[w] = __ldg(keyw + w);
-    __syncthreads();
     const uint64_t per = (total + gridDim.x - 1) / gridDim.x;
     const uint64_t c0 = per * blockIdx.x, c1 = c0 + per < total ? c0 + per : total;
     const uint32_t lane = threadIdx.x & 31;
@@ -66,7 +72,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     bool have = false;
     uint4 v = make_uint4(0, 0, 0, 0);
     uint4* op = nullptr;
-    const uint4* kp = nullptr;
+    uint32_t kb = 0;
     auto fetch = [&](uint64_t base) {
         while (base >= __ldg(&segs[seg].first) + __ldg(&segs[seg].n)) seg++;   // warp-uniform advance
         const uint64_t i = base + lane;
@@ -78,22 +84,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t local = i - __ldg(&sg->first);
         v = __ldcs(reinterpret_cast<const uint4*>(in_base + __ldg(&sg->in_off)) + local);
         op = reinterpret_cast<uint4*>(out_base + __ldg(&sg->out_off)) + local;
-        kp = reinterpret_cast<const uint4*>(skeys + 60u * __ldg(&sg->key));
+        kb = 60u * __ldg(&sg->key);
     };
     fetch(w0);
     while (w0 < c1) {
         const bool chave = have;
         const uint4 cv = v;
         uint4* const cop = op;
-        const uint4* const ckp = kp;
+        const uint32_t ckb = kb;
         w0 += blockDim.x;
         if (w0 < c1) fetch(w0);
         if (chave) {
-            const uint4 k0 = ckp[0];
-            uint32_t s0 = cv.x ^ k0.x, s1 = cv.y ^ k0.y, s2 = cv.z ^ k0.z, s3 = cv.w ^ k0.w;
+            uint32_t s0 = cv.x ^ keys.w[ckb], s1 = cv.y ^ keys.w[ckb + 1], s2 = cv.z ^ keys.w[ckb + 2],
+                     s3 = cv.w ^ keys.w[ckb + 3];
 #pragma unroll
-            for (int r = 1; r < NR; r++) t_round<DEC>(tb, s0, s1, s2, s3, KeyVec{ckp[r]});
-            __stcs(cop, final_round<DEC>(tb, s0, s1, s2, s3, KeyVec{ckp[NR]}));
+            for (int r = 1; r < NR; r++) t_round<DEC>(tb, s0, s1, s2, s3, KeyParamAt<KCAP>{keys, ckb + 4u * r});
+            __stcs(cop, final_round<DEC>(tb, s0, s1, s2, s3, KeyParamAt<KCAP>{keys, ckb + 4u * NR}));
         }
     }
 }
@@ -136,35 +142,38 @@ extern "C" aes_status aes_ecb_batch(const aes_round_keys* keys, int nkeys, int d
     aes_status st;
     if ((st = check_device_ptr(in_base, dev))) return st;
     if (out_base != in_base && (st = check_device_ptr(out_base, dev))) return st;
+    const bool small = nkeys <= 16;
     const void* f = nullptr;
-    if (nr == 10) f = decrypt ? (const void*)&batch_kernel<10, true> : (const void*)&batch_kernel<10, false>;
-    else if (nr == 12) f = decrypt ? (const void*)&batch_kernel<12, true> : (const void*)&batch_kernel<12, false>;
-    else f = decrypt ? (const void*)&batch_kernel<14, true> : (const void*)&batch_kernel<14, false>;
-    KernelInfo ki{f, (decrypt ? kSmemReplDec : kSmemReplEnc) + 240 * kBatchMaxKeys};
+#define AES_PICK_BATCH(K)                                                                                   \
+    f = nr == 10 ? (decrypt ? (const void*)&batch_kernel<10, true, K> : (const void*)&batch_kernel<10, false, K>) \
+      : nr == 12 ? (decrypt ? (const void*)&batch_kernel<12, true, K> : (const void*)&batch_kernel<12, false, K>) \
+                 : (decrypt ? (const void*)&batch_kernel<14, true, K> : (const void*)&batch_kernel<14, false, K>)
+    if (small) AES_PICK_BATCH(16); else AES_PICK_BATCH(kBatchMaxKeys);
+#undef AES_PICK_BATCH
+    const size_t smem = decrypt ? kSmemReplDec : kSmemReplEnc;
+    KernelInfo ki{f, smem};
     if ((st = resident_ctas(dev, ki, &occ, &nsm))) return st;
-    const size_t smem = (decrypt ? kSmemReplDec : kSmemReplEnc) + 240ull * nkeys;
-    // descriptors: segments, then 60 key words per key (ek or dk), in one
-    // stream-ordered allocation that is freed after the kernel on `stream`
-    const size_t seg_bytes = sizeof(BatchSeg) * nsegs, key_bytes = 240ull * nkeys;
-    std::vector<char> host(seg_bytes + key_bytes);
-    std::memcpy(host.data(), hs.data(), seg_bytes);
-    for (int k = 0; k < nkeys; k++)
-        std::memcpy(host.data() + seg_bytes + 240ull * k, decrypt ? keys[k].dk : keys[k].ek, 240);
+    // segment descriptors: one stream-ordered allocation freed after the kernel
+    const size_t seg_bytes = sizeof(BatchSeg) * nsegs;
     cudaStream_t cs = (cudaStream_t)stream;
     cudaMemPool_t pool;
     if ((st = desc_pool(dev, &pool))) return st;
     void* d = nullptr;
-    if ((e = cudaMallocFromPoolAsync(&d, host.size(), pool, cs)) != cudaSuccess) return cuda_fail(e);
-    if ((e = cudaMemcpyAsync(d, host.data(), host.size(), cudaMemcpyHostToDevice, cs)) != cudaSuccess) {
+    if ((e = cudaMallocFromPoolAsync(&d, seg_bytes, pool, cs)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaMemcpyAsync(d, hs.data(), seg_bytes, cudaMemcpyHostToDevice, cs)) != cudaSuccess) {
         cudaFreeAsync(d, cs);
         return cuda_fail(e);
     }
+    // key schedules by value (kernel parameters)
+    static thread_local BatchKeys<kBatchMaxKeys> kbig;
+    BatchKeys<16> ksmall;
+    uint32_t* kw = small ? ksmall.w : kbig.w;
+    for (int k = 0; k < nkeys; k++) std::memcpy(kw + 60 * k, decrypt ? keys[k].dk : keys[k].ek, 240);
     const char* pin = static_cast<const char*>(in_base);
     char* pout = static_cast<char*>(out_base);
     const BatchSeg* dsegs = static_cast<const BatchSeg*>(d);
-    const uint32_t* dkeys = reinterpret_cast<const uint32_t*>(static_cast<char*>(d) + seg_bytes);
-    void* args[] = {(void*)&pin, (void*)&pout, (void*)&dsegs, (void*)&nsegs, (void*)&total, (void*)&dkeys,
-                    (void*)&nkeys};
+    void* args[] = {(void*)&pin, (void*)&pout, (void*)&dsegs, (void*)&nsegs, (void*)&total,
+                    small ? (void*)&ksmall : (void*)&kbig};
     uint64_t want = (total + 31) / 32, cap = (uint64_t)nsm * occ;
     e = cudaLaunchKernel(f, dim3((unsigned)(want < cap ? want : cap)), dim3(kThreads), args, smem, cs);
     cudaError_t e2 = cudaFreeAsync(d, cs);
