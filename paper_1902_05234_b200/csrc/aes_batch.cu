@@ -142,13 +142,13 @@ extern "C" aes_status aes_ecb_batch(const aes_round_keys* keys, int nkeys, int d
     aes_status st;
     if ((st = check_device_ptr(in_base, dev))) return st;
     if (out_base != in_base && (st = check_device_ptr(out_base, dev))) return st;
-    const bool small = nkeys <= 16;
+    const int kcap = nkeys <= 16 ? 16 : nkeys <= 64 ? 64 : kBatchMaxKeys;   // parameter bytes scale with the tier
     const void* f = nullptr;
 #define AES_PICK_BATCH(K)                                                                                   \
     f = nr == 10 ? (decrypt ? (const void*)&batch_kernel<10, true, K> : (const void*)&batch_kernel<10, false, K>) \
       : nr == 12 ? (decrypt ? (const void*)&batch_kernel<12, true, K> : (const void*)&batch_kernel<12, false, K>) \
                  : (decrypt ? (const void*)&batch_kernel<14, true, K> : (const void*)&batch_kernel<14, false, K>)
-    if (small) AES_PICK_BATCH(16); else AES_PICK_BATCH(kBatchMaxKeys);
+    if (kcap == 16) AES_PICK_BATCH(16); else if (kcap == 64) AES_PICK_BATCH(64); else AES_PICK_BATCH(kBatchMaxKeys);
 #undef AES_PICK_BATCH
     const size_t smem = decrypt ? kSmemReplDec : kSmemReplEnc;
     KernelInfo ki{f, smem};
@@ -165,15 +165,16 @@ extern "C" aes_status aes_ecb_batch(const aes_round_keys* keys, int nkeys, int d
         return cuda_fail(e);
     }
     // key schedules by value (kernel parameters)
-    static thread_local BatchKeys<kBatchMaxKeys> kbig;
+    static thread_local BatchKeys<kBatchMaxKeys> kbig;   // 30 KiB: off the stack
+    static thread_local BatchKeys<64> kmid;
     BatchKeys<16> ksmall;
-    uint32_t* kw = small ? ksmall.w : kbig.w;
+    uint32_t* kw = kcap == 16 ? ksmall.w : kcap == 64 ? kmid.w : kbig.w;
     for (int k = 0; k < nkeys; k++) std::memcpy(kw + 60 * k, decrypt ? keys[k].dk : keys[k].ek, 240);
     const char* pin = static_cast<const char*>(in_base);
     char* pout = static_cast<char*>(out_base);
     const BatchSeg* dsegs = static_cast<const BatchSeg*>(d);
     void* args[] = {(void*)&pin, (void*)&pout, (void*)&dsegs, (void*)&nsegs, (void*)&total,
-                    small ? (void*)&ksmall : (void*)&kbig};
+                    kcap == 16 ? (void*)&ksmall : kcap == 64 ? (void*)&kmid : (void*)&kbig};
     uint64_t want = (total + 31) / 32, cap = (uint64_t)nsm * occ;
     e = cudaLaunchKernel(f, dim3((unsigned)(want < cap ? want : cap)), dim3(kThreads), args, smem, cs);
     cudaError_t e2 = cudaFreeAsync(d, cs);
