@@ -1,7 +1,8 @@
 """CPU parity oracle for the B200 AES-ECB path -- TEST INFRASTRUCTURE ONLY.
 
-Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
-and ``--impl reference`` legs may import this package.  The product package
+Only ``tests/`` (including ``tests/golden/make_samples.py``, which writes the
+golden samples the bench/tool parity gates read), ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` and ``--impl reference`` legs may import this package.  The product package
 ``paper_1902_05234_b200`` never imports it, and this package imports nothing
 from the product.
 

@@ -24,7 +24,8 @@
  *
  * Parity pins: tests/test_oracle_pins.py (GF worked examples of PAPER.md
  * Eqs 7-17, exhaustive field checks, S-box closed-form values, FIPS-197
- * App A/B/C, SP 800-38A F.1, OpenSSL cross-check).  No function here is
+ * App A/B/C, SP 800-38A F.1 (ECB), F.5 (CTR), F.2 (CBC), OpenSSL cross-checks,
+ * the InvCipher trace against the forward trace).  No function here is
  * "parity unpinned".
  */
 #include <stdint.h>
