@@ -426,7 +426,11 @@ def run_ours(a):
             "GBps": gbps / 8, "enc_ms": enc_ms, "dec_ms": dec_ms,
             "enc_Gbps": 8 * nbytes / (enc_ms * 1e-3) / 1e9, "dec_Gbps": 8 * nbytes / (dec_ms * 1e-3) / 1e9,
             "hbm_frac_step": (32.0 * n * 2 * K / (ms_local * 1e-3) / 1e9) / peak,
-            "roofline": roof, "roofline_lds": roof_lds, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "roofline_lds": roof_lds,
+            "roofline_note": ("T-table AES does 16*Nr shared-memory lookups per 32 HBM bytes, so the binding "
+                              "roofline is the shared-memory gather rate (roofline_lds), not HBM; T-table "
+                              "AES-128 cannot exceed ~28% of HBM on B200 (DESIGN.md 6, 11)"),
+            "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clocks, "gpu_launches": 2 * K, "gpu": torch.cuda.get_device_name(dev),
         }
         print(json.dumps(line), flush=True)
