@@ -315,8 +315,14 @@ def main():
     ldsp = lds_peak(s)
     record(what="peaks", hbm_gbs=hbm, lds_lookups_per_s=ldsp, gpu=torch.cuda.get_device_name(0))
     todo = ["variants", "config3", "modes", "sizes", "ladder", "batch"] if a.what == "all" else [a.what]
+    from bench import ClockSampler
+    clk = ClockSampler(torch.cuda.current_device())
+    clk.start()
+    clk.mark_start()
     for w in todo:
         globals()[w](a, s, hbm, ldsp)
+    clk.mark_end()
+    record(what="clocks", **clk.stop())
 
 
 if __name__ == "__main__":
