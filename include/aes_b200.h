@@ -151,12 +151,16 @@ aes_status aes_ecb_batch(const aes_round_keys *keys, int nkeys, int decrypt, con
  *  AES_VAR_SMEM_PLAIN : one copy of each table in shared memory (Li et al.,
  *                       PAPER.md:41); data-dependent bank conflicts.
  *  AES_VAR_CONST      : tables in __constant__ memory (the paper's choice,
- *                       PAPER.md:443); serialises divergent addresses. */
+ *                       PAPER.md:443); serialises divergent addresses.
+ *  AES_VAR_SMEM_REPL_TMA : as SMEM_REPL, with the input states staged into
+ *                       shared memory by bulk copies (cp.async.bulk + mbarrier)
+ *                       in a 2-stage ring per warp.  states_per_thread must be 1. */
 typedef enum {
     AES_VAR_DEFAULT = 0,
     AES_VAR_SMEM_REPL = 1,
     AES_VAR_SMEM_PLAIN = 2,
-    AES_VAR_CONST = 3
+    AES_VAR_CONST = 3,
+    AES_VAR_SMEM_REPL_TMA = 4
 } aes_variant;
 
 typedef struct {

@@ -78,7 +78,7 @@ constexpr size_t kSmemReplEnc = 2 * kRegion;
 constexpr size_t kSmemReplDec = 2 * kRegion + 255 * 256 + 128;
 constexpr size_t kSmemPlain = (4 * 256 + 256) * 4;
 
-enum { V_REPL = 1, V_PLAIN = 2, V_CONST = 3 };
+enum { V_REPL = 1, V_PLAIN = 2, V_CONST = 3, V_REPL_TMA = 4 };
 
 // ---------------------------------------------------------------------------
 // Table access policies: t(i, s, k) = T_i[byte k of s];  si(s, k) = Si4[byte k of s]

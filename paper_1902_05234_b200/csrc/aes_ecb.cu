@@ -159,6 +159,89 @@ __global__ void __launch_bounds__(kThreads, 1) lds_gather_kernel(uint32_t* sink,
 }
 
 // ---------------------------------------------------------------------------
+// AES_VAR_SMEM_REPL_TMA: the same rounds, with the states staged into shared
+// memory by the bulk-copy engine (cp.async.bulk + mbarrier, SASS UBLKCP) --
+// the north star's "TMA or cp.async staging of input tiles" (SURVEY.md 7 step
+// 5(e)).  Each warp owns a 2-stage ring of 512-byte tiles (32 states): lane 0
+// issues the copy of the tile two trips ahead, all lanes wait on the tile's
+// mbarrier, read their state with one LDS.128, cipher it, store with STG.128.
+// Kept as a measured variant: the tile still has to reach registers through
+// the shared-memory data path the rounds saturate.
+// ---------------------------------------------------------------------------
+constexpr int kTmaStages = 2;
+constexpr size_t kTmaTileBytes = 512;
+constexpr size_t kTmaRing = (kThreads / 32) * kTmaStages * kTmaTileBytes;   // 32 KiB
+constexpr size_t kTmaBars = (kThreads / 32) * kTmaStages * 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int NR, bool DEC>
+__global__ void __launch_bounds__(kThreads, 1)
+    ecb_tma_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n, const __grid_constant__ RK rk) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    const Tab<V_REPL> tb = Tab<V_REPL>::template setup<DEC>(smem);
+    const size_t tab_bytes = DEC ? kSmemReplDec : kSmemReplEnc;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    char* ring = reinterpret_cast<char*>(smem) + tab_bytes + warp * kTmaStages * kTmaTileBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + tab_bytes + kTmaRing) +
+                     warp * kTmaStages;
+    if (lane == 0) {
+        for (int st = 0; st < kTmaStages; st++)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + st)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const uint64_t total_warps = (uint64_t)gridDim.x * (kThreads / 32);
+    const uint64_t chunks = (n + 31) / 32;
+    const uint64_t q0 = (uint64_t)blockIdx.x * (kThreads / 32) + warp;
+    auto issue = [&](uint64_t k) {            // lane 0: tile of this warp's k-th chunk -> stage k % S
+        const uint64_t q = q0 + k * total_warps;
+        if (q >= chunks) return;
+        const uint64_t b0 = q * 32;
+        const uint32_t bytes = (uint32_t)((n - b0 < 32 ? n - b0 : 32) * 16);
+        const int st = (int)(k % kTmaStages);
+        const uint32_t bar = smem_u32(bars + st), dst = smem_u32(ring + st * kTmaTileBytes);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+            "l"(in + b0), "r"(bytes), "r"(bar)
+            : "memory");
+    };
+    if (lane == 0)
+        for (int k = 0; k < kTmaStages; k++) issue(k);
+    for (uint64_t k = 0;; k++) {
+        const uint64_t q = q0 + k * total_warps;
+        if (q >= chunks) break;
+        const int st = (int)(k % kTmaStages);
+        const uint32_t parity = (uint32_t)((k / kTmaStages) & 1);
+        const uint32_t bar = smem_u32(bars + st);
+        uint32_t done = 0;
+        while (!done)
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(bar), "r"(parity)
+                : "memory");
+        const uint64_t i = q * 32 + lane;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (i < n) v = reinterpret_cast<const uint4*>(ring + st * kTmaTileBytes)[lane];
+        uint32_t s0 = v.x ^ rk.w[0], s1 = v.y ^ rk.w[1], s2 = v.z ^ rk.w[2], s3 = v.w ^ rk.w[3];
+        // every lane has consumed the tile (the XOR used the loaded registers): recycle the stage
+        asm volatile("" ::"r"(s0), "r"(s1), "r"(s2), "r"(s3) : "memory");
+        __syncwarp();
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(k + kTmaStages);
+        }
+#pragma unroll
+        for (int r = 1; r < NR; r++) t_round<DEC>(tb, s0, s1, s2, s3, KeyAt{rk, r});
+        if (i < n) __stcs(out + i, final_round<DEC>(tb, s0, s1, s2, s3, KeyAt{rk, NR}));
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Host side: kernel registry and launch
 // ---------------------------------------------------------------------------
 
@@ -177,6 +260,9 @@ KernelInfo pick_spt(int v, int spt) {
             case 4: return kinfo<NR, DEC, V_REPL, 4>();
         }
     } else if (spt == 1) {
+        if (v == V_REPL_TMA)
+            return {reinterpret_cast<const void*>(&ecb_tma_kernel<NR, DEC>),
+                    (DEC ? kSmemReplDec : kSmemReplEnc) + kTmaRing + kTmaBars};
         if (v == V_PLAIN) return kinfo<NR, DEC, V_PLAIN, 1>();
         if (v == V_CONST) return kinfo<NR, DEC, V_CONST, 1>();
     }

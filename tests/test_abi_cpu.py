@@ -119,6 +119,8 @@ def test_validation_errors_before_any_cuda_call():
     assert _call(rk, 10, A, A, 4, cfg=cfg) == _native.AES_EVARIANT
     cfg = _native.aes_launch_config(_native.AES_VAR_SMEM_REPL, 3, 0, 0)
     assert _call(rk, 10, A, A, 4, cfg=cfg) == _native.AES_EVARIANT
+    cfg = _native.aes_launch_config(_native.AES_VAR_SMEM_REPL_TMA, 2, 0, 0)
+    assert _call(rk, 10, A, A, 4, cfg=cfg) == _native.AES_EVARIANT
     cfg = _native.aes_launch_config(_native.AES_VAR_SMEM_REPL, 1, -1, 0)
     assert _call(rk, 10, A, A, 4, cfg=cfg) == _native.AES_ERANGE
     # a tampered schedule (keybits inconsistent with nr) is rejected
