@@ -154,13 +154,17 @@ aes_status aes_ecb_batch(const aes_round_keys *keys, int nkeys, int decrypt, con
  *                       PAPER.md:443); serialises divergent addresses.
  *  AES_VAR_SMEM_REPL_TMA : as SMEM_REPL, with the input states staged into
  *                       shared memory by bulk copies (cp.async.bulk + mbarrier)
- *                       in a 2-stage ring per warp.  states_per_thread must be 1. */
+ *                       in a 2-stage ring per warp.  states_per_thread must be 1.
+ *  AES_VAR_SMEM_ROT   : ONE lane-replicated table (Te0 / Td0) and the other three
+ *                       as funnel-shift rotations (Eqs 23-25 are byte rotations
+ *                       of Eq 22): 64 KiB of shared memory instead of 128/192. */
 typedef enum {
     AES_VAR_DEFAULT = 0,
     AES_VAR_SMEM_REPL = 1,
     AES_VAR_SMEM_PLAIN = 2,
     AES_VAR_CONST = 3,
-    AES_VAR_SMEM_REPL_TMA = 4
+    AES_VAR_SMEM_REPL_TMA = 4,
+    AES_VAR_SMEM_ROT = 5
 } aes_variant;
 
 typedef struct {

@@ -15,13 +15,13 @@ from __future__ import annotations
 import ctypes
 
 from . import _native
-from ._native import (AES_VAR_CONST, AES_VAR_DEFAULT, AES_VAR_SMEM_PLAIN, AES_VAR_SMEM_REPL, AES_VAR_SMEM_REPL_TMA,
+from ._native import (AES_VAR_CONST, AES_VAR_DEFAULT, AES_VAR_SMEM_PLAIN, AES_VAR_SMEM_REPL, AES_VAR_SMEM_REPL_TMA, AES_VAR_SMEM_ROT,
                       aes_launch_config, aes_round_keys, status_string)
 
 __all__ = ["RoundKeys", "expand_key", "ecb_encrypt", "ecb_decrypt", "ecb", "ecb_batch", "ecb_batch_offsets", "KeySet", "ctr_xcrypt", "cbc_decrypt",
            "ecb_trace", "Pipeline",
            "lds_gather", "AesError", "AES_VAR_DEFAULT", "AES_VAR_SMEM_REPL", "AES_VAR_SMEM_PLAIN",
-           "AES_VAR_CONST", "AES_VAR_SMEM_REPL_TMA", "abi_version"]
+           "AES_VAR_CONST", "AES_VAR_SMEM_REPL_TMA", "AES_VAR_SMEM_ROT", "abi_version"]
 
 
 class AesError(RuntimeError):

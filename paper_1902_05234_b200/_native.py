@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_HERE, "libaes_b200.so")
 AES_OK, AES_EKEYBITS, AES_ENR, AES_ENULL, AES_EALIGN, AES_EOVERLAP, AES_ERANGE, \
     AES_ENOTDEVICE, AES_ECUDA, AES_EVARIANT = range(10)
 
-AES_VAR_DEFAULT, AES_VAR_SMEM_REPL, AES_VAR_SMEM_PLAIN, AES_VAR_CONST, AES_VAR_SMEM_REPL_TMA = range(5)
+AES_VAR_DEFAULT, AES_VAR_SMEM_REPL, AES_VAR_SMEM_PLAIN, AES_VAR_CONST, AES_VAR_SMEM_REPL_TMA, AES_VAR_SMEM_ROT = range(6)
 
 # every symbol include/aes_b200.h declares
 EXPORTS = ("aes_expand_key", "aes_ecb_encrypt", "aes_ecb_decrypt", "aes_ecb_launch",

@@ -77,8 +77,9 @@ constexpr uint32_t kOffSi = 2 * kRegion;
 constexpr size_t kSmemReplEnc = 2 * kRegion;
 constexpr size_t kSmemReplDec = 2 * kRegion + 255 * 256 + 128;
 constexpr size_t kSmemPlain = (4 * 256 + 256) * 4;
+constexpr size_t kSmemRot = 255 * 256 + 256;   // one replicated table (+ Si4 for decryption) in a 64 KiB region
 
-enum { V_REPL = 1, V_PLAIN = 2, V_CONST = 3, V_REPL_TMA = 4 };
+enum { V_REPL = 1, V_PLAIN = 2, V_CONST = 3, V_REPL_TMA = 4, V_ROT = 5 };
 
 // ---------------------------------------------------------------------------
 // Table access policies: t(i, s, k) = T_i[byte k of s];  si(s, k) = Si4[byte k of s]
@@ -120,6 +121,43 @@ struct Tab<V_REPL> {
                 int x = q >> 3, part = q & 7;
                 uint32_t u = __ldg(g_tab.si4 + x);
                 s4[(kOffSi + x * 256) / 16 + part] = make_uint4(u, u, u, u);
+            }
+        }
+        __syncthreads();
+        Tab tb;
+        tb.sb = reinterpret_cast<const char*>(smem);
+        tb.lo = (threadIdx.x & 31) * 4;
+        return tb;
+    }
+};
+
+// One lane-replicated table T0 (Td0) and T_i[x] = rotl(T0[x], 8i) computed by a
+// funnel shift per lookup ("a single Te0 x 32 replicas
+// plus __byte_perm / funnel-shift rotations"): 4x less shared memory, one more
+// ALU op for 3 of every 4 lookups.  Si4 sits in the other half of each row.
+template <>
+struct Tab<V_ROT> {
+    const char* sb;
+    uint32_t lo;
+    __device__ __forceinline__ uint32_t t(int i, uint32_t s, int k) const {
+        const uint32_t v = *reinterpret_cast<const uint32_t*>(sb + __byte_perm(lo, s, 0x1140 + 16 * k));
+        return i ? __funnelshift_l(v, v, 8 * i) : v;
+    }
+    __device__ __forceinline__ uint32_t si(uint32_t s, int k) const {
+        return *reinterpret_cast<const uint32_t*>(sb + 128 + __byte_perm(lo, s, 0x1140 + 16 * k));
+    }
+    template <bool DEC>
+    __device__ __forceinline__ static Tab setup(uint32_t* smem) {
+        const uint32_t* src = DEC ? &g_tab.td[0][0] : &g_tab.te[0][0];
+        uint4* s4 = reinterpret_cast<uint4*>(smem);
+#pragma unroll
+        for (int it = 0; it < 2048 / kThreads; it++) {     // 256 rows x 8 uint4 of T0
+            int q = threadIdx.x + it * kThreads, x = q >> 3, part = q & 7;
+            uint32_t v = __ldg(src + x);
+            s4[x * 16 + part] = make_uint4(v, v, v, v);
+            if (DEC) {
+                uint32_t u = __ldg(g_tab.si4 + x);
+                s4[x * 16 + 8 + part] = make_uint4(u, u, u, u);
             }
         }
         __syncthreads();

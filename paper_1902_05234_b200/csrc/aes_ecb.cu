@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int NR, bool DEC, int V, int SPT>
 KernelInfo kinfo() {
-    size_t sm = V == V_REPL ? (DEC ? kSmemReplDec : kSmemReplEnc) : V == V_PLAIN ? kSmemPlain : 0;
+    size_t sm = V == V_REPL ? (DEC ? kSmemReplDec : kSmemReplEnc) : V == V_PLAIN ? kSmemPlain : V == V_ROT ? kSmemRot : 0;
     return {reinterpret_cast<const void*>(&ecb_kernel<NR, DEC, V, SPT>), sm};
 }
 
@@ -264,6 +264,7 @@ KernelInfo pick_spt(int v, int spt) {
             return {reinterpret_cast<const void*>(&ecb_tma_kernel<NR, DEC>),
                     (DEC ? kSmemReplDec : kSmemReplEnc) + kTmaRing + kTmaBars};
         if (v == V_PLAIN) return kinfo<NR, DEC, V_PLAIN, 1>();
+        if (v == V_ROT) return kinfo<NR, DEC, V_ROT, 1>();
         if (v == V_CONST) return kinfo<NR, DEC, V_CONST, 1>();
     }
     return {nullptr, 0};

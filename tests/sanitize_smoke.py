@@ -22,7 +22,7 @@ for kb in (128, 256):
         x = torch.empty(16 * n, dtype=torch.uint8, device="cuda")
         synth.fill_device(x)
         host = synth.blocks(0, n)
-        variants = [(1, 1), (1, 2), (1, 4), (2, 1), (3, 1), (4, 1)]
+        variants = [(1, 1), (1, 2), (1, 4), (2, 1), (3, 1), (4, 1), (5, 1)]
         if os.environ.get("AES_SANITIZE_VARIANTS"):
             variants = [tuple(int(x) for x in p.split(":")) for p in os.environ["AES_SANITIZE_VARIANTS"].split(",")]
         for v, spt in variants:

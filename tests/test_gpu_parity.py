@@ -18,7 +18,7 @@ import oracle
 import synth
 from conftest import golden
 
-VARIANTS = [(1, 1), (1, 2), (1, 4), (2, 1), (3, 1), (4, 1)]   # (variant, states_per_thread)
+VARIANTS = [(1, 1), (1, 2), (1, 4), (2, 1), (3, 1), (4, 1), (5, 1)]   # (variant, states_per_thread)
 SIZES = [1, 2, 31, 32, 33, 1023, 1024, 1025, 4096 + 17, 148 * 1024 + 7, 65536]
 
 

@@ -152,11 +152,11 @@ def variants(a, s, hbm, ldsp):
     n = nbytes // 16
     key = synth.key(128)
     rk = aes.expand_key(key)
-    names = {1: "smem_repl", 2: "smem_plain", 3: "const (paper)", 4: "smem_repl + TMA staging"}
+    names = {1: "smem_repl", 2: "smem_plain", 3: "const (paper)", 4: "smem_repl + TMA staging", 5: "one table + rotations"}
     for kind in ("random", "zeros", "repeat", "ascii"):
         synth.fill_device(x, kind=kind)
-        for v, spt in ((1, 1), (1, 2), (1, 4), (4, 1), (2, 1), (3, 1)):
-            if kind != "random" and (v == 1 and spt != 1 or v == 4):
+        for v, spt in ((1, 1), (1, 2), (1, 4), (4, 1), (5, 1), (2, 1), (3, 1)):
+            if kind != "random" and (v == 1 and spt != 1 or v in (4, 5)):
                 continue
             for dec in (False, True):
                 f = (lambda: aes.ecb(rk, x, dec, out=out, variant=v, states_per_thread=spt))
