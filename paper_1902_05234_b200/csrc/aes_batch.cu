@@ -160,9 +160,9 @@ extern "C" aes_status aes_ecb_batch(const aes_round_keys* keys, int nkeys, int d
     if ((st = desc_pool(dev, &pool))) return st;
     void* d = nullptr;
     if ((e = cudaMallocFromPoolAsync(&d, seg_bytes, pool, cs)) != cudaSuccess) return cuda_fail(e);
-    if ((e = cudaMemcpyAsync(d, hs.data(), seg_bytes, cudaMemcpyHostToDevice, cs)) != cudaSuccess) {
+    if ((st = stage_h2d(dev, d, hs.data(), seg_bytes, cs))) {
         cudaFreeAsync(d, cs);
-        return cuda_fail(e);
+        return st;
     }
     // key schedules by value (kernel parameters)
     static thread_local BatchKeys<kBatchMaxKeys> kbig;   // 30 KiB: off the stack

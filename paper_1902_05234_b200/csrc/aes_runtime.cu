@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 #include <mutex>
 
 #include "aes_b200.h"
@@ -79,6 +80,37 @@ aes_status desc_pool(int dev, cudaMemPool_t* out) {
         g_pool[dev] = p;
     }
     *out = g_pool[dev];
+    return AES_OK;
+}
+
+// Per-thread, per-device page-locked staging buffer for small host->device
+// descriptor copies: cudaMemcpyAsync from pageable memory is synchronous,
+// from pinned memory it is a plain async DMA.  An event recorded after each
+// copy guards the buffer's reuse by the next call from the same thread.
+struct Staging {
+    void* host = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+};
+thread_local Staging t_stage[kMaxDev];
+
+aes_status stage_h2d(int dev, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (dev < 0 || dev >= kMaxDev) return AES_ERANGE;
+    Staging& st = t_stage[dev];
+    cudaError_t e;
+    if (st.ev && (e = cudaEventSynchronize(st.ev)) != cudaSuccess) return cuda_fail(e);
+    if (st.cap < bytes) {
+        if (st.host) cudaFreeHost(st.host);
+        st.host = nullptr;
+        st.cap = 0;
+        size_t cap = bytes < (64u << 10) ? (64u << 10) : 2 * bytes;
+        if ((e = cudaHostAlloc(&st.host, cap, cudaHostAllocDefault)) != cudaSuccess) return cuda_fail(e);
+        st.cap = cap;
+    }
+    if (!st.ev && (e = cudaEventCreateWithFlags(&st.ev, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e);
+    std::memcpy(st.host, src, bytes);
+    if ((e = cudaMemcpyAsync(dst, st.host, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaEventRecord(st.ev, s)) != cudaSuccess) return cuda_fail(e);
     return AES_OK;
 }
 
