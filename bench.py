@@ -215,8 +215,112 @@ def ncu_traffic(alg_bytes):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def _parity_gate(aes, golden, rk, x, ct, pt, s, first, n, dev, rank):
+    """No timing record without parity.  Expected values at
+    sampled global block indices come from tests/golden/samples.txt (written by
+    the oracle, tests/golden/make_samples.py); the oracle itself only runs in
+    the cpu_baseline / reference legs.  Returns True on success."""
+    import torch
+    with torch.cuda.stream(s):
+        aes.ecb_encrypt(rk, x, out=ct)
+        aes.ecb_decrypt(rk, ct, out=pt)
+    s.synchronize()
+
+    def gather(t):
+        return lambda loc: t.view(-1, 16)[torch.from_numpy(loc).to(dev)].cpu().numpy()
+
+    try:
+        ok = bool(torch.equal(pt, x))                                     # D(E(x)) == x on the whole shard
+        checked = golden.check("ecb_enc", KEYBITS, first, n, gather(ct))  # E(x_i) vs oracle samples
+        with torch.cuda.stream(s):
+            aes.ecb_decrypt(rk, x, out=pt)                                # D(x_i) vs oracle samples
+        s.synchronize()
+        checked += golden.check("ecb_dec", KEYBITS, first, n, gather(pt))
+        return ok and checked >= 6
+    except AssertionError as e:
+        print(f"[rank {rank}] {e}", file=sys.stderr)
+        return False
+
+
+def _lds_ceiling(aes, s, nsm, dev):
+    """The binding roofline, measured live: conflict-free 1-PRMT LDS gathers (lookups/s)."""
+    import torch
+    sink = torch.empty(nsm * 1024, dtype=torch.int32, device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        aes.lds_gather(sink, nsm, 64)
+        e0.record(s)
+        looks = aes.lds_gather(sink, nsm, 4096)
+        e1.record(s)
+    s.synchronize()
+    return looks / (e0.elapsed_time(e1) * 1e-3)
+
+
+def _e2e(aes, pdist, key, rk, x, ct, pt, nbytes, K, dev):
+    """The same metric through the C ABI with HOST buffers (aes_pipeline_run):
+    every step copies its inputs H2D from pinned memory and its results D2H.
+    Also measures the path's own roofline: the host link with H2D and D2H at once."""
+    import torch
+    hx = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    hx.copy_(x.cpu())
+    hc = torch.empty_like(hx).pin_memory()
+    hp = torch.empty_like(hx).pin_memory()
+    pipe = aes.Pipeline(chunk_bytes=64 << 20, depth=4)
+    pipe.run(rk, hx, hc)
+    pipe.run(rk, hc, hp, decrypt=True)
+    KE = max(1, min(K, 5))
+    pdist.barrier(dev)
+    t0 = time.perf_counter()
+    for _ in range(KE):
+        r = aes.expand_key(key)
+        pipe.run(r, hx, hc)
+        pipe.run(r, hc, hp, decrypt=True)
+    dt = pdist.max_over_ranks(time.perf_counter() - t0, dev)
+    pipe.close()
+    assert torch.equal(hp, hx)
+    s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    tl = []
+    for _ in range(3):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        with torch.cuda.stream(s1):
+            pt.copy_(hx, non_blocking=True)
+        with torch.cuda.stream(s2):
+            hp.copy_(ct, non_blocking=True)
+        torch.cuda.synchronize(dev)
+        tl.append(time.perf_counter() - t0)
+    link = nbytes / min(tl) / 1e9
+    return {"value": 8 * pdist.sum_over_ranks(2.0 * nbytes * KE, dev) / dt / 1e9, "unit": "Gbps",
+            "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": 2 * nbytes,
+            "steps": KE, "timing": "host perf_counter around synchronous aes_pipeline_run calls, max over ranks",
+            "path": "aes_pipeline_run: pinned host -> H2D -> kernel -> D2H, 64 MiB chunks x 4 streams",
+            "link_GBps_each_direction": link,
+            "link_frac": (2.0 * nbytes * KE / dt / 1e9) / link}   # bytes each way per second / ceiling
+
+
+def _rooflines(n, enc_ms, dec_ms, lds_peak, nsm, clocks):
+    """roofline (HBM, the BASELINE metric's denominator) and roofline_lds (the
+    binding one) of the dominant kernel, from its event-timed average launch."""
+    peak, peak_src, _ = measured_peaks()
+    kern_ms = max(enc_ms, dec_ms)
+    dom = "encrypt" if enc_ms >= dec_ms else "decrypt"
+    achieved = 32.0 * n / (kern_ms * 1e-3) / 1e9               # GB/s, 16 B read + 16 B written per block
+    traffic, traffic_src = ncu_traffic(32 * n)
+    lookups = 16 * NR * n
+    lds_nominal = nsm * 32 * (clocks.get("sm_mhz") or 1965.0) * 1e6
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "kernel": f"ecb_kernel<10,{dom}> (aes_ecb_{dom})", "kernel_ms": kern_ms,
+            "peak_source": peak_src, "algorithmic_bytes_per_launch": 32 * n, "traffic_source": traffic_src}
+    rate = lookups / (kern_ms * 1e-3)
+    roof_lds = {"bound": "smem_lookup", "achieved": rate / 1e12, "peak": lds_peak / 1e12, "unit": "Tlookup/s",
+                "frac": rate / lds_peak,
+                "peak_source": "aes_mb_lds_gather measured in this run (conflict-free 1-PRMT LDS gathers)",
+                "nominal_peak": lds_nominal / 1e12, "frac_of_nominal": rate / lds_nominal,
+                "lookups_per_launch": lookups}
+    return roof, roof_lds, peak
+
+
 def run_ours(a):
-    import numpy as np
     import torch
 
     from paper_1902_05234_b200 import dist as pdist
@@ -235,13 +339,13 @@ def run_ours(a):
     pdist.barrier(dev)
     import paper_1902_05234_b200 as aes   # ImportError if libaes_b200.so is still missing
     import synth
+    from synth import golden
 
     nbytes = (a.bytes_per_gpu // 16) * 16
     n = nbytes // 16
     first = rank * n                      # this rank's slice of the global stream
     key = synth.key(KEYBITS)
     rk = aes.expand_key(key)
-
     x = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     ct = torch.empty_like(x)
     pt = torch.empty_like(x)
@@ -250,54 +354,21 @@ def run_ours(a):
         synth.fill_device(x, first_block=first)
     s.synchronize()
 
-    # ---- parity gate (no timing record without parity) -------
-    # Expected values at sampled global block indices come from
-    # tests/golden/samples.txt (written by the oracle, tests/golden/make_samples.py);
-    # the oracle itself only runs in the cpu_baseline / reference legs.
-    from synth import golden
-    with torch.cuda.stream(s):
-        aes.ecb_encrypt(rk, x, out=ct)
-        aes.ecb_decrypt(rk, ct, out=pt)
-    s.synchronize()
-
-    def gather(t):
-        return lambda loc: t.view(-1, 16)[torch.from_numpy(loc).to(dev)].cpu().numpy()
-
-    try:
-        ok = bool(torch.equal(pt, x))                                   # D(E(x)) == x on the whole shard
-        checked = golden.check("ecb_enc", KEYBITS, first, n, gather(ct))  # E(x_i) vs oracle samples
-        with torch.cuda.stream(s):
-            aes.ecb_decrypt(rk, x, out=pt)                              # D(x_i) vs oracle samples
-        s.synchronize()
-        checked += golden.check("ecb_dec", KEYBITS, first, n, gather(pt))
-        ok = ok and checked >= 6
-    except AssertionError as e:
-        print(f"[rank {rank}] {e}", file=sys.stderr)
-        ok = False
-    bad = pdist.sum_over_ranks(0.0 if ok else 1.0, dev)
-    if bad:
+    ok = _parity_gate(aes, golden, rk, x, ct, pt, s, first, n, dev, rank)
+    if pdist.sum_over_ranks(0.0 if ok else 1.0, dev):
         if rank == 0:
             print(json.dumps({"metric": METRIC, "error": "parity failed; no timing recorded"}), flush=True)
         return 1
 
-    # ---- LDS-gather ceiling, measured live (binding roofline) --------------
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    sink = torch.empty(nsm * 1024, dtype=torch.int32, device=dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(s):
-        aes.lds_gather(sink, nsm, 64)
-        e0.record(s)
-        looks = aes.lds_gather(sink, nsm, 4096)
-        e1.record(s)
-    s.synchronize()
-    lds_peak = looks / (e0.elapsed_time(e1) * 1e-3)          # lookups / s
+    lds_peak = _lds_ceiling(aes, s, nsm, dev)
 
-    # ---- step ------------------------------------------------------------
+    # ---- the step: A1/A2 on the host, then the two kernels -----------------
     nvtx = torch.cuda.nvtx
 
     def step(ev=None):
         nvtx.range_push("aes step")
-        r = aes.expand_key(key)                               # A1/A2 (host)
+        r = aes.expand_key(key)
         if ev:
             ev[0].record(s)
         nvtx.range_push("aes_ecb_encrypt")
@@ -342,69 +413,10 @@ def run_ours(a):
     dec_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
     total_payload = pdist.sum_over_ranks(2.0 * nbytes * K, dev)
     gbps = 8 * total_payload / (ms * 1e-3) / 1e9
+    assert torch.equal(pt, x)             # decrypt(encrypt(x)) == x after the timed region too
 
-    # sanity after the timed region: decrypt(encrypt(x)) == x still
-    assert torch.equal(pt, x)
-
-    # ---- e2e: same metric through the C ABI with HOST buffers ------------
-    e2e = None
-    if not a.no_e2e:
-        hx = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
-        hx.copy_(x.cpu())
-        hc = torch.empty_like(hx).pin_memory()
-        hp = torch.empty_like(hx).pin_memory()
-        pipe = aes.Pipeline(chunk_bytes=64 << 20, depth=4)
-        pipe.run(rk, hx, hc)
-        pipe.run(rk, hc, hp, decrypt=True)
-        KE = max(1, min(K, 5))
-        pdist.barrier(dev)
-        t0 = time.perf_counter()
-        for _ in range(KE):
-            r = aes.expand_key(key)
-            pipe.run(r, hx, hc)
-            pipe.run(r, hc, hp, decrypt=True)
-        dt = pdist.max_over_ranks(time.perf_counter() - t0, dev)
-        pipe.close()
-        assert torch.equal(hp, hx)
-        # the path's own roofline: the host link with H2D and D2H running at once
-        s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-        tl = []
-        for _ in range(3):
-            torch.cuda.synchronize(dev)
-            t0 = time.perf_counter()
-            with torch.cuda.stream(s1):
-                pt.copy_(hx, non_blocking=True)
-            with torch.cuda.stream(s2):
-                hp.copy_(ct, non_blocking=True)
-            torch.cuda.synchronize(dev)
-            tl.append(time.perf_counter() - t0)
-        link = nbytes / min(tl) / 1e9
-        e2e = {"value": 8 * pdist.sum_over_ranks(2.0 * nbytes * KE, dev) / dt / 1e9, "unit": "Gbps",
-               "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": 2 * nbytes,
-               "steps": KE, "timing": "host perf_counter around synchronous aes_pipeline_run calls, max over ranks",
-               "path": "aes_pipeline_run: pinned host -> H2D -> kernel -> D2H, 64 MiB chunks x 4 streams",
-               "link_GBps_each_direction": link,
-               "link_frac": (2.0 * nbytes * KE / dt / 1e9) / link}   # bytes each way per second / ceiling
-
-    # ---- roofline of the dominant kernel ---------------------------------
-    peak, peak_src, peaks = measured_peaks()
-    kern_ms = max(enc_ms, dec_ms)
-    dom = "encrypt" if enc_ms >= dec_ms else "decrypt"
-    achieved = 32.0 * n / (kern_ms * 1e-3) / 1e9               # GB/s, 16 B read + 16 B written per block
-    traffic, traffic_src = ncu_traffic(32 * n)
-    lookups = 16 * NR * n
-    sm_clk = clocks.get("sm_mhz") or 1965.0
-    lds_nominal = nsm * 32 * sm_clk * 1e6
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": f"ecb_kernel<10,{dom}> (aes_ecb_{dom})", "kernel_ms": kern_ms,
-            "peak_source": peak_src, "algorithmic_bytes_per_launch": 32 * n,
-            "traffic_source": traffic_src}
-    roof_lds = {"bound": "smem_lookup", "achieved": lookups / (kern_ms * 1e-3) / 1e12,
-                "peak": lds_peak / 1e12, "unit": "Tlookup/s",
-                "frac": (lookups / (kern_ms * 1e-3)) / lds_peak,
-                "peak_source": "aes_mb_lds_gather measured in this run (conflict-free 1-PRMT LDS gathers)",
-                "nominal_peak": lds_nominal / 1e12, "frac_of_nominal": (lookups / (kern_ms * 1e-3)) / lds_nominal,
-                "lookups_per_launch": lookups}
+    e2e = None if a.no_e2e else _e2e(aes, pdist, key, rk, x, ct, pt, nbytes, K, dev)
+    roof, roof_lds, peak = _rooflines(n, enc_ms, dec_ms, lds_peak, nsm, clocks)
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -413,6 +425,7 @@ def run_ours(a):
         cpu = {"value": g, "unit": "Gbps", "cores": cores, "kind": "oracle", "sample": sample, "cpu": cpu_model()}
 
     if rank == 0:
+        l2 = torch.cuda.get_device_properties(dev).L2_cache_size
         line = {
             "metric": METRIC, "value": gbps, "unit": "Gbps", "n_gpus": world, "steps": K, "warmup": a.warmup,
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -421,7 +434,8 @@ def run_ours(a):
                        "keybits": KEYBITS, "bytes_per_gpu": nbytes,
                        "global_bytes": nbytes * world, "parallelism": f"dp{world} (contiguous block shards)",
                        "step": f"expand_key + encrypt({nbytes / GIB:g} GiB) + decrypt({nbytes / GIB:g} GiB)",
-                       "l2": "inputs (1 GiB) larger than L2 (126 MB); no flush",
+                       "l2": (f"inputs ({nbytes / 2**20:.0f} MiB) larger than L2 ({l2 / 2**20:.0f} MiB); no flush"
+                              if nbytes > l2 else "inputs smaller than L2 (harness-test size): L2-warm"),
                        "variant": "smem_repl, 1 state/thread, persistent grid"},
             "GBps": gbps / 8, "enc_ms": enc_ms, "dec_ms": dec_ms,
             "enc_Gbps": 8 * nbytes / (enc_ms * 1e-3) / 1e9, "dec_Gbps": 8 * nbytes / (dec_ms * 1e-3) / 1e9,
