@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(kThreads, 1) mixed(const uint32_t* __restrict_
 template <int KIND, int E>
 float run(const uint32_t* gtab, cudaTextureObject_t tex, uint32_t* sink, int grid, int iters) {
     cudaFuncSetAttribute((const void*)mixed<KIND, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 32 * 4);
+    cudaGetLastError();
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -55,9 +56,10 @@ float run(const uint32_t* gtab, cudaTextureObject_t tex, uint32_t* sink, int gri
         cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms, e0, e1);
     }
+    cudaError_t err = cudaGetLastError();
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    return ms;
+    return err == cudaSuccess ? ms : -(float)err;
 }
 
 extern "C" int mixed_run(const uint32_t* gtab, uint32_t* sink, int grid, int iters, float* out) {

@@ -23,4 +23,4 @@ rc = L.mixed_run(tab.data_ptr(), sink.data_ptr(), nsm, 1024, out)
 names = ["16 LDS", "16 LDS + 2 LDS", "16 LDS + 4 LDS", "16 LDS + 2 LDG(L1)", "16 LDS + 4 LDG(L1)",
          "16 LDS + 2 TEX", "16 LDS + 4 TEX"]
 for nm, ms in zip(names, out):
-    print(json.dumps({"kernel": nm, "ms": ms, "rel_to_16_lds": ms / out[0], "rc": rc}))
+    print(json.dumps({"kernel": nm, "ms": ms, "rel_to_16_lds": ms / out[0] if out[0] > 0 else None, "rc": rc}))
