@@ -12,7 +12,7 @@ template <int KIND, int E>
 __global__ void __launch_bounds__(kThreads, 1) mixed(const uint32_t* __restrict__ gtab, cudaTextureObject_t tex,
                                                       uint32_t* sink, int iters) {
     extern __shared__ __align__(16) uint32_t smem[];
-    for (int w = threadIdx.x; w < 256 * 32; w += blockDim.x) smem[w] = w * 2654435761u;
+    for (int w = threadIdx.x; w < 256 * 64; w += blockDim.x) smem[w] = w * 2654435761u;
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31;
     const char* sb = reinterpret_cast<const char*>(smem);
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kThreads, 1) mixed(const uint32_t* __restrict_
 
 template <int KIND, int E>
 float run(const uint32_t* gtab, cudaTextureObject_t tex, uint32_t* sink, int grid, int iters) {
-    cudaFuncSetAttribute((const void*)mixed<KIND, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 32 * 4);
+    cudaFuncSetAttribute((const void*)mixed<KIND, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
     cudaGetLastError();
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
@@ -51,7 +51,7 @@ float run(const uint32_t* gtab, cudaTextureObject_t tex, uint32_t* sink, int gri
     float ms = 0;
     for (int r = 0; r < 2; r++) {
         cudaEventRecord(e0);
-        mixed<KIND, E><<<grid, kThreads, 256 * 32 * 4>>>(gtab, tex, sink, iters);
+        mixed<KIND, E><<<grid, kThreads, 65536>>>(gtab, tex, sink, iters);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms, e0, e1);
