@@ -1,5 +1,9 @@
-// aes_ecb.cu -- sm_100a AES-ECB kernels (steps A4..A10 of SURVEY.md 8(a)) and
-// the device entry points of the C ABI (include/aes_b200.h).
+// aes_ecb.cu -- sm_100a AES kernels (steps A4..A10 of SURVEY.md 8(a)): ECB,
+// CTR and CBC-decryption, the table-placement / staging ablation variants,
+// the per-round trace and the LDS-gather microbenchmark, with their C ABI
+// entry points (include/aes_b200.h).  The building blocks every kernel shares
+// (tables, table policies, the Eq 26 round, the final round) are in
+// aes_device.cuh.
 //
 // One 16-byte state per thread (sec 4.1), held in four
 // 32-bit registers (column c = LE word c).  Rounds are the paper's T-table
