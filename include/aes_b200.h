@@ -190,7 +190,7 @@ aes_status aes_ecb_launch(const aes_round_keys *rk, int nr, int decrypt, const v
  * complete (synchronous).  in_host/out_host: host memory, 16*nblocks bytes,
  * ideally page-locked (pageable memory works but does not overlap);
  * in_host == out_host allowed.  chunk_bytes: multiple of 16, >= 16; depth 1..8.
- * Messages up to 1 MiB whose host buffers are both page-locked and mapped
+ * Messages up to 8 MiB whose host buffers are both page-locked and mapped
  * (e.g. cudaHostAlloc / torch pin_memory) skip the staging: the kernel reads
  * and writes them over the link directly (one launch, no copies).
  * A pipeline object is not re-entrant (its staging buffers are shared): use

@@ -11,7 +11,7 @@
 using namespace aesb200;
 
 namespace {
-constexpr uint64_t kZeroCopyMax = 1ull << 20;
+constexpr uint64_t kZeroCopyMax = 8ull << 20;
 
 // Device address of a page-locked, mapped host pointer (nullptr otherwise).
 const void* mapped(const void* host) {
