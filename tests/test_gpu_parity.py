@@ -486,3 +486,22 @@ def test_cli_file_round_trip(aes, tmp_path):
     padded0 = np.zeros(16 * n, np.uint8)
     padded0[:len(data)] = np.frombuffer(data, np.uint8)
     assert enc.read_bytes() == oracle.ctr(key, iv, padded0, nthreads=8).tobytes()[:len(data)]
+
+
+def test_pipeline_zero_copy_and_staged_paths(aes):
+    """Pinned messages <= 8 MiB run on mapped host memory (zero copy), larger
+    ones through the chunked staging; both equal the oracle."""
+    key = synth.key(128)
+    rk = aes.expand_key(key)
+    p = aes.Pipeline(chunk_bytes=1 << 20, depth=3)
+    for n in ((8 << 20) // 16, (8 << 20) // 16 + 1, (9 << 20) // 16 + 7):
+        host = synth.blocks(0, n)
+        src = torch.from_numpy(host.copy()).pin_memory()
+        dst = torch.empty_like(src).pin_memory()
+        p.run(rk, src, dst)
+        idx = np.r_[0:64, n // 2:n // 2 + 64, n - 64:n]
+        want = oracle.encrypt(key, host.reshape(-1, 16)[idx].copy().reshape(-1), nthreads=8)
+        assert np.array_equal(dst.numpy().reshape(-1, 16)[idx].reshape(-1), want), n
+        p.run(rk, dst, dst, decrypt=True)
+        assert np.array_equal(dst.numpy(), host), n
+    p.close()
