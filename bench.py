@@ -396,6 +396,7 @@ def run_ours(a):
     time.sleep(0.3)
     pdist.barrier(dev)
     torch.cuda.synchronize(dev)
+    wall0 = time.perf_counter()
     clk.mark_start()
     with torch.cuda.stream(s):
         t_start.record(s)
@@ -406,6 +407,7 @@ def run_ours(a):
     clk.mark_end()
     torch.cuda.synchronize(dev)
     pdist.barrier(dev)
+    wall_ms = 1e3 * (time.perf_counter() - wall0)   # includes rank skew
     clocks = clk.stop()
     ms_local = t_start.elapsed_time(t_end)
     ms = pdist.max_over_ranks(ms_local, dev)
@@ -449,6 +451,7 @@ def run_ours(a):
                               "AES-128 cannot exceed ~28% of HBM on B200 (DESIGN.md 6, 11)"),
             "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clocks, "gpu_launches": 2 * K, "gpu": torch.cuda.get_device_name(dev),
+            "wall_window_ms_rank0": wall_ms,
         }
         print(json.dumps(line), flush=True)
     return 0
