@@ -130,7 +130,7 @@ class ClockSampler:
     window is shorter than the sampling period)."""
     Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,temperature.gpu")
 
     def __init__(self, gpu_index: int):
         self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
@@ -168,12 +168,12 @@ class ClockSampler:
         rows = []
         for ln in open(self.path):
             f = [x.strip() for x in ln.split(",")]
-            if len(f) < 10:
+            if len(f) < 11:
                 continue
             try:
                 ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
                 rows.append((ts, float(f[2]), float(f[3]), float(f[4]),
-                             [n for n, v in zip(names, f[6:10]) if v.lower().startswith("active")]))
+                             [n for n, v in zip(names, f[6:10]) if v.lower().startswith("active")], float(f[10])))
             except ValueError:
                 continue
         os.unlink(self.path)
@@ -186,7 +186,7 @@ class ClockSampler:
             inside = sorted(rows, key=lambda r: abs(r[0] - mid))[:3]
         return {"sm_mhz": statistics.median(r[1] for r in inside), "sm_max_mhz": max(r[2] for r in inside),
                 "reasons": sorted({x for r in inside for x in r[4]}), "samples": len(inside),
-                "power_w_max": max(r[3] for r in inside), "window": window}
+                "power_w_max": max(r[3] for r in inside), "temp_c_max": max(r[5] for r in inside), "window": window}
 
 
 def measured_peaks():
