@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "aes_b200.h"
@@ -107,6 +108,73 @@ __global__ void __launch_bounds__(kThreads, 1)
     ctr_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n, const __grid_constant__ RK rk,
                const __grid_constant__ ModeP mp) {
     aes_body<NR, false, V_REPL, 1, M_CTR>(in, out, n, rk, mp);
+}
+
+// CTR with counter-mode caching (Bernstein-Schwabe): the counters of 256
+// consecutive blocks differ only in byte 15 (row 3 of column 3), so in round 1
+// only column 0 depends on it (one Te3 lookup) and in round 2 each column has
+// exactly one varying input byte (four lookups); everything else is a
+// per-256-block-group constant (8 words: P0, e1..e3 of round 1 and Q0..Q3 of
+// round 2).  Each trip a CTA's 1024 blocks span at most 5 groups: 5 lanes of
+// warp 0 compute their constants into a double-buffered shared-memory table,
+// and every block then needs 1 + 4 + 16*(NR-3) + 16 lookups instead of 16*NR
+// (133 vs 160 for AES-128).
+constexpr int kCtrGroups = 5;
+constexpr size_t kCtrTableBytes = 2 * 8 * 8 * 4;   // 2 buffers x 8 groups x 8 words
+
+template <int NR>
+__global__ void __launch_bounds__(kThreads, 1)
+    ctr_cached_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n,
+                      const __grid_constant__ RK rk, const __grid_constant__ ModeP mp) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    const Tab<V_REPL> tb = Tab<V_REPL>::template setup<false>(smem);
+    uint32_t* gtab = smem + kSmemReplEnc / 4;
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    int buf = 0;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += T, buf ^= 1) {   // CTA-uniform
+        const uint64_t lo_b = mp.ctr_lo + base;
+        const uint64_t hi_b = mp.ctr_hi + (lo_b < mp.ctr_lo ? 1ull : 0ull);
+        uint32_t* g = gtab + buf * 64;
+        const uint64_t i = base + threadIdx.x;
+        uint4 p = make_uint4(0, 0, 0, 0);
+        if (i < n) p = __ldcs(in + i);
+        if (threadIdx.x < kCtrGroups) {
+            const uint64_t g0 = lo_b & ~0xffull;
+            const uint64_t glo = g0 + 256ull * threadIdx.x;
+            const uint64_t ghi = hi_b + (glo < g0 ? 1ull : 0ull);
+            // representative counter of the group (byte 15 = 0), round 0
+            const uint32_t s0 = __byte_perm((uint32_t)(ghi >> 32), 0, 0x0123) ^ rk.w[0];
+            const uint32_t s1 = __byte_perm((uint32_t)ghi, 0, 0x0123) ^ rk.w[1];
+            const uint32_t s2 = __byte_perm((uint32_t)(glo >> 32), 0, 0x0123) ^ rk.w[2];
+            const uint32_t s3 = __byte_perm((uint32_t)glo, 0, 0x0123) ^ rk.w[3];
+            // round 1: e1..e3 do not see byte 15; e0 = P0 ^ Te3[byte 3 of s3]
+            const uint32_t P0 = tb.t(0, s0, 0) ^ tb.t(1, s1, 1) ^ tb.t(2, s2, 2) ^ rk.w[4];
+            const uint32_t e1 = tb.t(0, s1, 0) ^ tb.t(1, s2, 1) ^ tb.t(2, s3, 2) ^ tb.t(3, s0, 3) ^ rk.w[5];
+            const uint32_t e2 = tb.t(0, s2, 0) ^ tb.t(1, s3, 1) ^ tb.t(2, s0, 2) ^ tb.t(3, s1, 3) ^ rk.w[6];
+            const uint32_t e3 = tb.t(0, s3, 0) ^ tb.t(1, s0, 1) ^ tb.t(2, s1, 2) ^ tb.t(3, s2, 3) ^ rk.w[7];
+            // round 2: f_j = Q_j ^ (the one lookup of a byte of e0)
+            const uint32_t Q0 = tb.t(1, e1, 1) ^ tb.t(2, e2, 2) ^ tb.t(3, e3, 3) ^ rk.w[8];
+            const uint32_t Q1 = tb.t(0, e1, 0) ^ tb.t(1, e2, 1) ^ tb.t(2, e3, 2) ^ rk.w[9];
+            const uint32_t Q2 = tb.t(0, e2, 0) ^ tb.t(1, e3, 1) ^ tb.t(3, e1, 3) ^ rk.w[10];
+            const uint32_t Q3 = tb.t(0, e3, 0) ^ tb.t(2, e1, 2) ^ tb.t(3, e2, 3) ^ rk.w[11];
+            uint4* gw = reinterpret_cast<uint4*>(g + 8 * threadIdx.x);
+            gw[0] = make_uint4(P0, e1, e2, e3);
+            gw[1] = make_uint4(Q0, Q1, Q2, Q3);
+        }
+        __syncthreads();   // table of this trip ready; buffer `buf` is rewritten two trips later
+        if (i < n) {
+            const uint32_t off = (uint32_t)(lo_b & 0xff) + threadIdx.x;   // < 256 + 1024
+            const uint4* c = reinterpret_cast<const uint4*>(g + 8 * (off >> 8));
+            const uint4 c0 = c[0], c1 = c[1];
+            const uint32_t x = (off & 0xff) ^ (rk.w[3] >> 24);              // byte 15 of this counter ^ k0
+            const uint32_t e0 = c0.x ^ tb.t(3, x << 24, 3);
+            uint32_t f0 = c1.x ^ tb.t(0, e0, 0), f1 = c1.y ^ tb.t(3, e0, 3);
+            uint32_t f2 = c1.z ^ tb.t(2, e0, 2), f3 = c1.w ^ tb.t(1, e0, 1);
+#pragma unroll
+            for (int r = 3; r < NR; r++) t_round<false>(tb, f0, f1, f2, f3, KeyAt{rk, r});
+            __stcs(out + i, xor4(p, final_round<false>(tb, f0, f1, f2, f3, KeyAt{rk, NR})));
+        }
+    }
 }
 
 template <int NR>
@@ -286,9 +354,19 @@ KernelInfo pick(int nr, bool dec, int v, int spt) {
 KernelInfo pick_mode(int nr, int mode) {
     const void* f = nullptr;
     if (mode == M_CTR) {
-        f = nr == 10 ? (const void*)&ctr_kernel<10> : nr == 12 ? (const void*)&ctr_kernel<12>
-                                                               : (const void*)&ctr_kernel<14>;
-        return {f, kSmemReplEnc};
+        // AES_B200_CTR_KERNEL=plain selects the uncached kernel (A/B measurement only)
+        static const bool plain = [] {
+            const char* e = std::getenv("AES_B200_CTR_KERNEL");
+            return e && std::strcmp(e, "plain") == 0;
+        }();
+        if (plain) {
+            f = nr == 10 ? (const void*)&ctr_kernel<10> : nr == 12 ? (const void*)&ctr_kernel<12>
+                                                                   : (const void*)&ctr_kernel<14>;
+            return {f, kSmemReplEnc};
+        }
+        f = nr == 10 ? (const void*)&ctr_cached_kernel<10> : nr == 12 ? (const void*)&ctr_cached_kernel<12>
+                                                                      : (const void*)&ctr_cached_kernel<14>;
+        return {f, kSmemReplEnc + kCtrTableBytes};
     }
     f = nr == 10 ? (const void*)&cbc_decrypt_kernel<10> : nr == 12 ? (const void*)&cbc_decrypt_kernel<12>
                                                                    : (const void*)&cbc_decrypt_kernel<14>;
