@@ -122,6 +122,31 @@ __global__ void __launch_bounds__(kThreads, 1)
 constexpr int kCtrGroups = 5;
 constexpr size_t kCtrTableBytes = 2 * 8 * 8 * 4;   // 2 buffers x 8 groups x 8 words
 
+// Group constants (8 words) of the 256-block counter group starting at the
+// 128-bit counter (ghi:glo) with byte 15 = 0.
+template <class TB>
+__device__ __forceinline__ void ctr_group_constants(const TB& tb, const RK& rk, uint64_t ghi, uint64_t glo,
+                                                    uint32_t* dst) {
+    // representative counter (byte 15 = 0), round 0
+    const uint32_t s0 = __byte_perm((uint32_t)(ghi >> 32), 0, 0x0123) ^ rk.w[0];
+    const uint32_t s1 = __byte_perm((uint32_t)ghi, 0, 0x0123) ^ rk.w[1];
+    const uint32_t s2 = __byte_perm((uint32_t)(glo >> 32), 0, 0x0123) ^ rk.w[2];
+    const uint32_t s3 = __byte_perm((uint32_t)glo, 0, 0x0123) ^ rk.w[3];
+    // round 1: e1..e3 do not see byte 15; e0 = P0 ^ Te3[byte 3 of s3]
+    const uint32_t P0 = tb.t(0, s0, 0) ^ tb.t(1, s1, 1) ^ tb.t(2, s2, 2) ^ rk.w[4];
+    const uint32_t e1 = tb.t(0, s1, 0) ^ tb.t(1, s2, 1) ^ tb.t(2, s3, 2) ^ tb.t(3, s0, 3) ^ rk.w[5];
+    const uint32_t e2 = tb.t(0, s2, 0) ^ tb.t(1, s3, 1) ^ tb.t(2, s0, 2) ^ tb.t(3, s1, 3) ^ rk.w[6];
+    const uint32_t e3 = tb.t(0, s3, 0) ^ tb.t(1, s0, 1) ^ tb.t(2, s1, 2) ^ tb.t(3, s2, 3) ^ rk.w[7];
+    // round 2: f_j = Q_j ^ (the one lookup of a byte of e0)
+    const uint32_t Q0 = tb.t(1, e1, 1) ^ tb.t(2, e2, 2) ^ tb.t(3, e3, 3) ^ rk.w[8];
+    const uint32_t Q1 = tb.t(0, e1, 0) ^ tb.t(1, e2, 1) ^ tb.t(2, e3, 2) ^ rk.w[9];
+    const uint32_t Q2 = tb.t(0, e2, 0) ^ tb.t(1, e3, 1) ^ tb.t(3, e1, 3) ^ rk.w[10];
+    const uint32_t Q3 = tb.t(0, e3, 0) ^ tb.t(2, e1, 2) ^ tb.t(3, e2, 3) ^ rk.w[11];
+    uint4* gw = reinterpret_cast<uint4*>(dst);
+    gw[0] = make_uint4(P0, e1, e2, e3);
+    gw[1] = make_uint4(Q0, Q1, Q2, Q3);
+}
+
 template <int NR>
 __global__ void __launch_bounds__(kThreads, 1)
     ctr_cached_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n,
@@ -130,41 +155,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     const Tab<V_REPL> tb = Tab<V_REPL>::template setup<false>(smem);
     uint32_t* gtab = smem + kSmemReplEnc / 4;
     const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
-    int buf = 0;
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += T, buf ^= 1) {   // CTA-uniform
+    // lane 0 of warps 0..4 each own one of the <= 5 groups a trip touches
+    const bool maker = (threadIdx.x & 31) == 0 && (threadIdx.x >> 5) < kCtrGroups;
+    const uint32_t gk = threadIdx.x >> 5;
+    auto make = [&](uint64_t base, int b) {   // table of the trip starting at block `base` into buffer b
         const uint64_t lo_b = mp.ctr_lo + base;
         const uint64_t hi_b = mp.ctr_hi + (lo_b < mp.ctr_lo ? 1ull : 0ull);
-        uint32_t* g = gtab + buf * 64;
+        const uint64_t g0 = lo_b & ~0xffull;
+        const uint64_t glo = g0 + 256ull * gk;
+        ctr_group_constants(tb, rk, hi_b + (glo < g0 ? 1ull : 0ull), glo, gtab + b * 64 + 8 * gk);
+    };
+    uint64_t base = (uint64_t)blockIdx.x * blockDim.x;
+    if (maker && base < n) make(base, 0);
+    __syncthreads();
+    // Software pipeline: while a trip's blocks are ciphered with table `buf`,
+    // the makers fill the other buffer for the next trip (read by nobody since
+    // the barrier that ended the trip before).
+    for (int buf = 0; base < n; base += T, buf ^= 1) {   // CTA-uniform
         const uint64_t i = base + threadIdx.x;
         uint4 p = make_uint4(0, 0, 0, 0);
         if (i < n) p = __ldcs(in + i);
-        if (threadIdx.x < kCtrGroups) {
-            const uint64_t g0 = lo_b & ~0xffull;
-            const uint64_t glo = g0 + 256ull * threadIdx.x;
-            const uint64_t ghi = hi_b + (glo < g0 ? 1ull : 0ull);
-            // representative counter of the group (byte 15 = 0), round 0
-            const uint32_t s0 = __byte_perm((uint32_t)(ghi >> 32), 0, 0x0123) ^ rk.w[0];
-            const uint32_t s1 = __byte_perm((uint32_t)ghi, 0, 0x0123) ^ rk.w[1];
-            const uint32_t s2 = __byte_perm((uint32_t)(glo >> 32), 0, 0x0123) ^ rk.w[2];
-            const uint32_t s3 = __byte_perm((uint32_t)glo, 0, 0x0123) ^ rk.w[3];
-            // round 1: e1..e3 do not see byte 15; e0 = P0 ^ Te3[byte 3 of s3]
-            const uint32_t P0 = tb.t(0, s0, 0) ^ tb.t(1, s1, 1) ^ tb.t(2, s2, 2) ^ rk.w[4];
-            const uint32_t e1 = tb.t(0, s1, 0) ^ tb.t(1, s2, 1) ^ tb.t(2, s3, 2) ^ tb.t(3, s0, 3) ^ rk.w[5];
-            const uint32_t e2 = tb.t(0, s2, 0) ^ tb.t(1, s3, 1) ^ tb.t(2, s0, 2) ^ tb.t(3, s1, 3) ^ rk.w[6];
-            const uint32_t e3 = tb.t(0, s3, 0) ^ tb.t(1, s0, 1) ^ tb.t(2, s1, 2) ^ tb.t(3, s2, 3) ^ rk.w[7];
-            // round 2: f_j = Q_j ^ (the one lookup of a byte of e0)
-            const uint32_t Q0 = tb.t(1, e1, 1) ^ tb.t(2, e2, 2) ^ tb.t(3, e3, 3) ^ rk.w[8];
-            const uint32_t Q1 = tb.t(0, e1, 0) ^ tb.t(1, e2, 1) ^ tb.t(2, e3, 2) ^ rk.w[9];
-            const uint32_t Q2 = tb.t(0, e2, 0) ^ tb.t(1, e3, 1) ^ tb.t(3, e1, 3) ^ rk.w[10];
-            const uint32_t Q3 = tb.t(0, e3, 0) ^ tb.t(2, e1, 2) ^ tb.t(3, e2, 3) ^ rk.w[11];
-            uint4* gw = reinterpret_cast<uint4*>(g + 8 * threadIdx.x);
-            gw[0] = make_uint4(P0, e1, e2, e3);
-            gw[1] = make_uint4(Q0, Q1, Q2, Q3);
-        }
-        __syncthreads();   // table of this trip ready; buffer `buf` is rewritten two trips later
+        if (maker && base + T < n) make(base + T, buf ^ 1);
         if (i < n) {
+            const uint64_t lo_b = mp.ctr_lo + base;
             const uint32_t off = (uint32_t)(lo_b & 0xff) + threadIdx.x;   // < 256 + 1024
-            const uint4* c = reinterpret_cast<const uint4*>(g + 8 * (off >> 8));
+            const uint4* c = reinterpret_cast<const uint4*>(gtab + buf * 64 + 8 * (off >> 8));
             const uint4 c0 = c[0], c1 = c[1];
             const uint32_t x = (off & 0xff) ^ (rk.w[3] >> 24);              // byte 15 of this counter ^ k0
             const uint32_t e0 = c0.x ^ tb.t(3, x << 24, 3);
@@ -174,6 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int r = 3; r < NR; r++) t_round<false>(tb, f0, f1, f2, f3, KeyAt{rk, r});
             __stcs(out + i, xor4(p, final_round<false>(tb, f0, f1, f2, f3, KeyAt{rk, NR})));
         }
+        __syncthreads();   // next table written, this one fully read
     }
 }
 
