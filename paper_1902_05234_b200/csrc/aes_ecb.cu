@@ -155,9 +155,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const Tab<V_REPL> tb = Tab<V_REPL>::template setup<false>(smem);
     uint32_t* gtab = smem + kSmemReplEnc / 4;
     const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
-    // lane 0 of warps 0..4 each own one of the <= 5 groups a trip touches
-    const bool maker = (threadIdx.x & 31) == 0 && (threadIdx.x >> 5) < kCtrGroups;
-    const uint32_t gk = threadIdx.x >> 5;
+    // lanes 0..4 of warp 0 each own one of the <= 5 groups a trip touches
+    // (one warp: the 27 lookups of a table are 27 LDS instructions for all 5 groups)
+    const bool maker = threadIdx.x < kCtrGroups;
+    const uint32_t gk = threadIdx.x;
     auto make = [&](uint64_t base, int b) {   // table of the trip starting at block `base` into buffer b
         const uint64_t lo_b = mp.ctr_lo + base;
         const uint64_t hi_b = mp.ctr_hi + (lo_b < mp.ctr_lo ? 1ull : 0ull);
