@@ -115,12 +115,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // only column 0 depends on it (one Te3 lookup) and in round 2 each column has
 // exactly one varying input byte (four lookups); everything else is a
 // per-256-block-group constant (8 words: P0, e1..e3 of round 1 and Q0..Q3 of
-// round 2).  Each trip a CTA's 1024 blocks span at most 5 groups: 5 lanes of
-// warp 0 compute their constants into a double-buffered shared-memory table,
-// and every block then needs 1 + 4 + 16*(NR-3) + 16 lookups instead of 16*NR
-// (133 vs 160 for AES-128).
-constexpr int kCtrGroups = 5;
-constexpr size_t kCtrTableBytes = 2 * 8 * 8 * 4;   // 2 buffers x 8 groups x 8 words
+// round 2), so every block needs 1 + 4 + 16*(NR-3) + 16 lookups instead of
+// 16*NR (133 vs 160 for AES-128).
+constexpr size_t kCtrTableBytes = (kThreads / 32) * 32 * 8 * 4;   // 32 warps x 32 entries x 8 words = 32 KiB
 
 // Group constants (8 words) of the 256-block counter group starting at the
 // 128-bit counter (ghi:glo) with byte 15 = 0.
@@ -153,36 +150,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const __grid_constant__ RK rk, const __grid_constant__ ModeP mp) {
     extern __shared__ __align__(16) uint32_t smem[];
     const Tab<V_REPL> tb = Tab<V_REPL>::template setup<false>(smem);
-    uint32_t* gtab = smem + kSmemReplEnc / 4;
+    // Warp-private table of group constants for the warp's next 16 trips x
+    // (the <= 2 groups its 32 consecutive blocks touch): 32 entries x 8 words,
+    // filled by the 32 lanes in parallel -- 27 LDS instructions per 16 trips
+    // and no block-wide barrier (warps drift freely, as in the ECB kernel).
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* wt = smem + kSmemReplEnc / 4 + warp * 256;
     const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
-    // lanes 0..4 of warp 0 each own one of the <= 5 groups a trip touches
-    // (one warp: the 27 lookups of a table are 27 LDS instructions for all 5 groups)
-    const bool maker = threadIdx.x < kCtrGroups;
-    const uint32_t gk = threadIdx.x;
-    auto make = [&](uint64_t base, int b) {   // table of the trip starting at block `base` into buffer b
-        const uint64_t lo_b = mp.ctr_lo + base;
-        const uint64_t hi_b = mp.ctr_hi + (lo_b < mp.ctr_lo ? 1ull : 0ull);
-        const uint64_t g0 = lo_b & ~0xffull;
-        const uint64_t glo = g0 + 256ull * gk;
-        ctr_group_constants(tb, rk, hi_b + (glo < g0 ? 1ull : 0ull), glo, gtab + b * 64 + 8 * gk);
-    };
-    uint64_t base = (uint64_t)blockIdx.x * blockDim.x;
-    if (maker && base < n) make(base, 0);
-    __syncthreads();
-    // Software pipeline: while a trip's blocks are ciphered with table `buf`,
-    // the makers fill the other buffer for the next trip (read by nobody since
-    // the barrier that ended the trip before).
-    for (int buf = 0; base < n; base += T, buf ^= 1) {   // CTA-uniform
-        const uint64_t i = base + threadIdx.x;
-        uint4 p = make_uint4(0, 0, 0, 0);
-        if (i < n) p = __ldcs(in + i);
-        if (maker && base + T < n) make(base + T, buf ^ 1);
+    const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + warp * 32;   // this warp's first block
+    for (uint64_t t = 0;; t++) {
+        const uint64_t cb = first + t * T;   // warp-uniform
+        if (cb >= n) break;
+        if ((t & 15) == 0) {
+            __syncwarp();                    // previous 16 trips' entries fully read
+            const uint64_t tcb = cb + (uint64_t)(lane >> 1) * T;
+            if (tcb < n) {
+                const uint64_t lo_c = mp.ctr_lo + tcb;
+                const uint64_t hi_c = mp.ctr_hi + (lo_c < mp.ctr_lo ? 1ull : 0ull);
+                const uint64_t g0 = lo_c & ~0xffull;
+                const uint64_t glo = g0 + 256ull * (lane & 1);
+                ctr_group_constants(tb, rk, hi_c + (glo < g0 ? 1ull : 0ull), glo, wt + 8 * lane);
+            }
+            __syncwarp();
+        }
+        const uint64_t i = cb + lane;
         if (i < n) {
-            const uint64_t lo_b = mp.ctr_lo + base;
-            const uint32_t off = (uint32_t)(lo_b & 0xff) + threadIdx.x;   // < 256 + 1024
-            const uint4* c = reinterpret_cast<const uint4*>(gtab + buf * 64 + 8 * (off >> 8));
+            const uint4 p = __ldcs(in + i);
+            const uint32_t off = (uint32_t)((mp.ctr_lo + cb) & 0xff) + lane;   // < 256 + 32
+            const uint4* c = reinterpret_cast<const uint4*>(wt + 8 * (2 * (uint32_t)(t & 15) + (off >> 8)));
             const uint4 c0 = c[0], c1 = c[1];
-            const uint32_t x = (off & 0xff) ^ (rk.w[3] >> 24);              // byte 15 of this counter ^ k0
+            const uint32_t x = (off & 0xff) ^ (rk.w[3] >> 24);                 // byte 15 of this counter ^ k0
             const uint32_t e0 = c0.x ^ tb.t(3, x << 24, 3);
             uint32_t f0 = c1.x ^ tb.t(0, e0, 0), f1 = c1.y ^ tb.t(3, e0, 3);
             uint32_t f2 = c1.z ^ tb.t(2, e0, 2), f3 = c1.w ^ tb.t(1, e0, 1);
@@ -190,7 +187,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int r = 3; r < NR; r++) t_round<false>(tb, f0, f1, f2, f3, KeyAt{rk, r});
             __stcs(out + i, xor4(p, final_round<false>(tb, f0, f1, f2, f3, KeyAt{rk, NR})));
         }
-        __syncthreads();   // next table written, this one fully read
     }
 }
 
