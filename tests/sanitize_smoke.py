@@ -33,6 +33,18 @@ for kb in (128, 256):
         aes.ecb_encrypt(rk, y, out=y)
         aes.ecb_decrypt(rk, y, out=y)
         ok &= bool(torch.equal(x, y))
+# CTR (counter-mode-cached kernel: warp-private group tables) and CBC decryption
+for kb in (128, 256):
+    key = synth.key(kb)
+    rk = aes.expand_key(key)
+    for n in (1, 300, 3 * 1024 + 17):
+        x = torch.empty(16 * n, dtype=torch.uint8, device="cuda")
+        synth.fill_device(x)
+        host = synth.blocks(0, n)
+        for iv in (bytes([0xFF] * 15 + [0xC8]), bytes(range(16))):
+            ok &= np.array_equal(aes.ctr_xcrypt(rk, iv, x, block_offset=77).cpu().numpy(),
+                                 oracle.ctr(key, iv, host, block_offset=77, nthreads=4))
+        ok &= np.array_equal(aes.cbc_decrypt(rk, bytes(16), x).cpu().numpy(), oracle.cbc(key, bytes(16), host, True))
 torch.cuda.synchronize()
 print("sanitize_smoke", "ok" if ok else "MISMATCH")
 sys.exit(0 if ok else 1)
