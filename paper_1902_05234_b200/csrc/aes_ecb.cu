@@ -190,29 +190,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-// CBC decryption, P_i = D(C_i) ^ C_{i-1}: a warp holds 32 consecutive
-// ciphertext blocks, so C_{i-1} comes from the neighbouring lane by four
-// shuffles; only lane 0 reads its predecessor (or the IV) from memory.
 template <int NR>
 __global__ void __launch_bounds__(kThreads, 1)
     cbc_decrypt_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n,
                        const __grid_constant__ RK rk, const __grid_constant__ ModeP mp) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    const Tab<V_REPL> tb = Tab<V_REPL>::template setup<true>(smem);
-    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
-    const uint32_t lane = threadIdx.x & 31;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i - lane < n; i += T) {   // warp-uniform
-        const bool live = i < n;
-        uint4 v = live ? __ldcs(in + i) : make_uint4(0, 0, 0, 0);
-        uint4 w;
-        w.x = __shfl_up_sync(0xffffffffu, v.x, 1);
-        w.y = __shfl_up_sync(0xffffffffu, v.y, 1);
-        w.z = __shfl_up_sync(0xffffffffu, v.z, 1);
-        w.w = __shfl_up_sync(0xffffffffu, v.w, 1);
-        if (lane == 0) w = i ? __ldg(in + i - 1) : make_uint4(mp.iv[0], mp.iv[1], mp.iv[2], mp.iv[3]);
-        v = cipher_block<NR, true>(tb, v, rk);
-        if (live) __stcs(out + i, xor4(v, w));
-    }
+    aes_body<NR, true, V_REPL, 1, M_CBCD>(in, out, n, rk, mp);
 }
 
 // Debug/pin kernel (aes_ecb_trace): the state after ARK(0) and `rounds` rounds
