@@ -448,7 +448,7 @@ def run_ours(a):
             "roofline": roof, "roofline_lds": roof_lds,
             "roofline_note": ("T-table AES does 16*Nr shared-memory lookups per 32 HBM bytes, so the binding "
                               "roofline is the shared-memory gather rate (roofline_lds), not HBM; T-table "
-                              "AES-128 cannot exceed ~28% of HBM on B200 (DESIGN.md 6, 11)"),
+                              "AES-128 ECB cannot exceed ~28% of HBM on B200 (DESIGN.md 6, 11)"),
             "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clocks, "gpu_launches": 2 * K, "gpu": torch.cuda.get_device_name(dev),
             "wall_window_ms_rank0": wall_ms,
