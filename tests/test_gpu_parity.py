@@ -505,3 +505,33 @@ def test_pipeline_zero_copy_and_staged_paths(aes):
         p.run(rk, dst, dst, decrypt=True)
         assert np.array_equal(dst.numpy(), host), n
     p.close()
+
+
+@pytest.mark.parametrize("keybits", [128, 256])
+def test_ctr_large_many_table_refreshes(aes, keybits):
+    """The cached CTR kernel refreshes its per-warp group tables every 16
+    trips: 80 MiB (> 32 trips per warp) with a block_offset that puts byte 15
+    mid-group, checked on sampled blocks against the oracle (incl. warp and
+    group boundaries) and by an on-device round trip."""
+    key = synth.key(keybits)
+    rk = aes.expand_key(key)
+    n = (80 << 20) // 16 + 13
+    x = _dev_rand(n, first=3)
+    iv = bytes([0xFF] * 8) + bytes([0x12, 0x34, 0x56, 0x78, 0xFF, 0xFF, 0xFF, 0xF0])
+    off = 2**64 - 1000
+    y = aes.ctr_xcrypt(rk, iv, x, block_offset=off)
+    rng = np.random.default_rng(keybits)
+    T = 148 * 1024
+    idx = np.unique(np.r_[0:40, 16 * T - 40:16 * T + 40, 32 * T - 3:32 * T + 3, n - 40:n, rng.integers(0, n, 2048)])
+    idx = idx[idx < n].astype(np.int64)
+    got = y.view(-1, 16)[torch.from_numpy(idx).cuda()].cpu().numpy()
+    plain = synth.blocks_at((idx + 3).astype(np.uint64))
+    for j, i in enumerate(idx):
+        want = oracle.ctr(key, iv, plain[j].copy(), block_offset=(off + int(i)) % 2**64)
+        # block_offset is 64-bit in the ABI: off + i wraps into the high counter half only via the counter add
+        if off + int(i) >= 2**64:
+            hi = int.from_bytes(iv, "big") + off + int(i)
+            want = oracle.ctr(key, (hi % 2**128).to_bytes(16, "big"), plain[j].copy())
+        assert np.array_equal(got[j], want), int(i)
+    back = aes.ctr_xcrypt(rk, iv, y, block_offset=off)
+    assert torch.equal(back, x)
