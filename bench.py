@@ -133,7 +133,8 @@ class ClockSampler:
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,temperature.gpu")
 
     def __init__(self, gpu_index: int):
-        self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
+        fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+        os.close(fd)
         self.gpu = gpu_index
         self.p = None
         self.t0 = self.t1 = None
