@@ -156,6 +156,10 @@ class ClockSampler:
 
     def stop(self):
         if not self.p:
+            try:
+                os.unlink(self.path)
+            except OSError:
+                pass
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.05)
         self.p.terminate()
