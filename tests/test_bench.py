@@ -13,6 +13,15 @@ KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "
         "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"}
 
 
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
 def _last_json(out):
     lines = [ln for ln in out.splitlines() if ln.startswith("{")]
     assert lines, out[-2000:]
@@ -47,7 +56,7 @@ def test_bench_our_arm_n1():
 def test_bench_n2_code_path_with_gloo_on_one_gpu():
     env = dict(os.environ, AES_BENCH_BACKEND="gloo")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                        "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
                         "--steps", "3", "--warmup", "3", "--bytes-per-gpu", str(32 << 20)],
                        cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
