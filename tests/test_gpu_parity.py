@@ -535,3 +535,18 @@ def test_ctr_large_many_table_refreshes(aes, keybits):
         assert np.array_equal(got[j], want), int(i)
     back = aes.ctr_xcrypt(rk, iv, y, block_offset=off)
     assert torch.equal(back, x)
+
+
+def test_config2_full_parity_every_byte(aes):
+    """BASELINE config 2 with FULL parity: all 67,108,864 blocks of the 1 GiB
+    AES-128 encryption compared with the oracle (threaded over all host cores),
+    in the bench's launch configuration."""
+    import os
+    n = (1 << 30) // 16
+    key = synth.key(128)
+    rk = aes.expand_key(key)
+    x = _dev_rand(n)
+    ct = aes.ecb_encrypt(rk, x).cpu().numpy()
+    want = oracle.encrypt(key, synth.blocks(0, n), nthreads=len(os.sched_getaffinity(0)))
+    bad = np.nonzero((ct.reshape(-1, 16) != want.reshape(-1, 16)).any(axis=1))[0]
+    assert bad.size == 0, f"{bad.size} blocks differ, first {int(bad[0])}"
