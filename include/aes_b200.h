@@ -99,6 +99,10 @@ aes_status aes_ecb_decrypt(const aes_round_keys *rk, int nr, const void *in, voi
  * (rank r of a multi-GPU job) continue the global counter stream.
  *  iv : host pointer to 16 bytes (initial counter block T_1), read during the call.
  *  in/out/nblocks/stream : as aes_ecb_encrypt (in == out allowed).
+ * Implementation: counter-mode caching -- the 256 counters of a group differ
+ * only in byte 15, so rounds 1-2 take 5 lookups instead of 32 per block
+ * (environment AES_B200_CTR_KERNEL=plain selects the uncached kernel, for A/B
+ * measurements only; results are identical).
  * Errors: as aes_ecb_encrypt, plus AES_ENULL for iv. */
 aes_status aes_ctr_xcrypt(const aes_round_keys *rk, int nr, const uint8_t *iv, uint64_t block_offset,
                           const void *in, void *out, uint64_t nblocks, void *stream);
