@@ -550,3 +550,24 @@ def test_config2_full_parity_every_byte(aes):
     want = oracle.encrypt(key, synth.blocks(0, n), nthreads=len(os.sched_getaffinity(0)))
     bad = np.nonzero((ct.reshape(-1, 16) != want.reshape(-1, 16)).any(axis=1))[0]
     assert bad.size == 0, f"{bad.size} blocks differ, first {int(bad[0])}"
+
+
+def test_ctr_plain_kernel_matches_cached(aes, tmp_path):
+    """AES_B200_CTR_KERNEL=plain (uncached A/B reference) gives the same bytes."""
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = (
+        "import sys; sys.path.insert(0, '.');"
+        "import torch, numpy as np, synth, paper_1902_05234_b200 as aes;"
+        "x = torch.empty(16 * 300007, dtype=torch.uint8, device='cuda'); synth.fill_device(x);"
+        "rk = aes.expand_key(synth.key(192));"
+        "np.save(sys.argv[1], aes.ctr_xcrypt(rk, bytes(range(16)), x, block_offset=251).cpu().numpy())")
+    outs = []
+    for env_val in ("plain", "cached"):
+        f = str(tmp_path / f"{env_val}.npy")
+        env = dict(__import__("os").environ, AES_B200_CTR_KERNEL=env_val)
+        r = subprocess.run([sys.executable, "-c", code, f], cwd=ROOT, env=env, capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
