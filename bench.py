@@ -459,6 +459,8 @@ def run_ours(a):
             "wall_window_ms_rank0": wall_ms,
         }
         print(json.dumps(line), flush=True)
+    pdist.barrier(dev)
+    pdist.finalize()
     return 0
 
 

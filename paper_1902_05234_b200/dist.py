@@ -69,3 +69,10 @@ def barrier(device=None):
             dist.barrier(device_ids=[device.index if hasattr(device, "index") else int(device)])
         else:
             dist.barrier()
+
+
+def finalize():
+    """Destroy the default process group if this module created one."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.destroy_process_group()
