@@ -97,10 +97,29 @@ __device__ __forceinline__ void aes_body(const uint4* __restrict__ in, uint4* __
     }
 }
 
+// ECB with the next trip's state load issued before the current trip's rounds
+// (software prefetch across loop iterations; the compiler does not hoist it).
+template <int NR, bool DEC, int V>
+__device__ __forceinline__ void ecb_prefetch_body(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n,
+                                                  const RK& rk) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    const Tab<V> tb = Tab<V>::template setup<DEC>(smem);
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (i < n) v = __ldcs(in + i);
+    for (; i < n; i += T) {
+        const uint4 cur = v;
+        if (i + T < n) v = __ldcs(in + i + T);
+        __stcs(out + i, cipher_block<NR, DEC>(tb, cur, rk));
+    }
+}
+
 template <int NR, bool DEC, int V, int SPT>
 __global__ void __launch_bounds__(kThreads, 1)
     ecb_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n, const __grid_constant__ RK rk) {
-    aes_body<NR, DEC, V, SPT, M_ECB>(in, out, n, rk, ModeP{});
+    if (SPT == 1 && V == V_REPL) ecb_prefetch_body<NR, DEC, V>(in, out, n, rk);
+    else aes_body<NR, DEC, V, SPT, M_ECB>(in, out, n, rk, ModeP{});
 }
 
 template <int NR>
