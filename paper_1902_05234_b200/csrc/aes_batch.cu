@@ -69,22 +69,47 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     // Software pipeline: the segment walk and the 128-bit load of the NEXT trip
     // are issued before the rounds of the current one, hiding their latency chain.
+    // The warp's current segment is cached in registers (first, end, offsets,
+    // key): while a message spans whole trips no descriptor is re-read.
     bool have = false;
     uint4 v = make_uint4(0, 0, 0, 0);
     uint4* op = nullptr;
     uint32_t kb = 0;
+    uint64_t sf = 0, se = 0, sin = 0, sout = 0;   // cached descriptor of segment `seg`
+    uint32_t skey = 0;
+    auto load_seg = [&]() {
+        const BatchSeg* sg = segs + seg;
+        sf = __ldg(&sg->first);
+        se = sf + __ldg(&sg->n);
+        sin = __ldg(&sg->in_off);
+        sout = __ldg(&sg->out_off);
+        skey = __ldg(&sg->key);
+    };
+    load_seg();
     auto fetch = [&](uint64_t base) {
-        while (base >= __ldg(&segs[seg].first) + __ldg(&segs[seg].n)) seg++;   // warp-uniform advance
+        if (base >= se) {                                   // warp-uniform advance
+            do { seg++; load_seg(); } while (base >= se);
+        }
         const uint64_t i = base + lane;
         have = i < c1;
         if (!have) return;
-        uint32_t sidx = seg;
-        while (i >= __ldg(&segs[sidx].first) + __ldg(&segs[sidx].n)) sidx++;
-        const BatchSeg* sg = segs + sidx;
-        const uint64_t local = i - __ldg(&sg->first);
-        v = __ldcs(reinterpret_cast<const uint4*>(in_base + __ldg(&sg->in_off)) + local);
-        op = reinterpret_cast<uint4*>(out_base + __ldg(&sg->out_off)) + local;
-        kb = 60u * __ldg(&sg->key);
+        uint64_t f = sf, io = sin, oo = sout;
+        uint32_t key = skey;
+        if (i >= se) {                                      // this lane runs past the warp's segment
+            uint32_t sidx = seg;
+            do {
+                sidx++;
+            } while (i >= __ldg(&segs[sidx].first) + __ldg(&segs[sidx].n));
+            const BatchSeg* sg = segs + sidx;
+            f = __ldg(&sg->first);
+            io = __ldg(&sg->in_off);
+            oo = __ldg(&sg->out_off);
+            key = __ldg(&sg->key);
+        }
+        const uint64_t local = i - f;
+        v = __ldcs(reinterpret_cast<const uint4*>(in_base + io) + local);
+        op = reinterpret_cast<uint4*>(out_base + oo) + local;
+        kb = 60u * key;
     };
     fetch(w0);
     while (w0 < c1) {
