@@ -87,8 +87,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     load_seg();
     auto fetch = [&](uint64_t base) {
-        if (base >= se) {                                   // warp-uniform advance
-            do { seg++; load_seg(); } while (base >= se);
+        if (base >= se) {   // warp-uniform advance: gallop then bisect over the sorted `first`s
+            uint32_t lo = seg + 1, step = 1;                // first[seg+1] == se <= base
+            while (lo + step < nsegs && __ldg(&segs[lo + step].first) <= base) {
+                lo += step;
+                step <<= 1;
+            }
+            uint32_t hi = lo + step < nsegs ? lo + step : nsegs;   // first[hi] > base (or hi == nsegs)
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (__ldg(&segs[mid].first) <= base) lo = mid; else hi = mid;
+            }
+            seg = lo;
+            load_seg();
         }
         const uint64_t i = base + lane;
         have = i < c1;
