@@ -58,10 +58,11 @@ def test_shard_range_partitions():
         shard_range(10, 2, 2)
 
 
-def test_two_rank_gloo_sharding_invariance():
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_sharding_invariance(world):
     import oracle
     import synth
-    world, n = 2, 1001
+    n = 1001
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -74,6 +75,6 @@ def test_two_rank_gloo_sharding_invariance():
         assert p.exitcode == 0
     whole = oracle.encrypt(synth.key(128), synth.blocks(0, n)).tobytes()
     assert b"".join(r[3] for r in res) == whole
-    assert [r[1:3] for r in res] == [(0, 500), (500, 1001)]
-    assert all(r[4] == 11.0 for r in res)        # MAX over ranks
-    assert all(r[5] == float(n) for r in res)    # SUM over ranks
+    assert [r[1:3] for r in res] == [shard_range(n, r, world) for r in range(world)]
+    assert all(r[4] == 10.0 + world - 1 for r in res)   # MAX over ranks
+    assert all(r[5] == float(n) for r in res)           # SUM over ranks
