@@ -94,10 +94,10 @@ aes_status aes_pipeline_run(aes_pipeline* p, const aes_round_keys* rk, int nr, i
     // reads and writes the host buffers directly over the link (zero copy) --
     // one launch instead of copy + launch + copy, which is what bounds the
     // paper's file sizes.  Both buffers must be mapped.
-    if (bytes <= kZeroCopyMax) {
+    if (bytes <= kZeroCopyMax && !(((uintptr_t)in_host | (uintptr_t)out_host) & 15)) {
         const void* din = mapped(in_host);
         void* dout = const_cast<void*>(mapped(out_host));
-        if (din && dout) {
+        if (din && dout && !(((uintptr_t)din | (uintptr_t)dout) & 15)) {
             st = launch_ecb(rk, nr, decrypt, din, dout, nblocks, p->st[0], false);
             if (st == AES_OK && (e = cudaStreamSynchronize(p->st[0])) != cudaSuccess) st = cuda_fail(e);
             if (prev != p->device) cudaSetDevice(prev);

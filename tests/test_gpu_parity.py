@@ -571,3 +571,20 @@ def test_ctr_plain_kernel_matches_cached(aes, tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(f))
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_pipeline_unaligned_host_buffers(aes):
+    """Host buffers need no alignment: a pinned buffer at an 8-byte offset takes
+    the staged path (the zero-copy path is only used for 16-byte-aligned ones)."""
+    key = synth.key(128)
+    rk = aes.expand_key(key)
+    n = 1000
+    host = synth.blocks(0, n)
+    big = torch.empty(16 * n + 16, dtype=torch.uint8).pin_memory()
+    src = big[8:8 + 16 * n]
+    src.copy_(torch.from_numpy(host))
+    dst = torch.empty(16 * n + 16, dtype=torch.uint8).pin_memory()[8:8 + 16 * n]
+    p = aes.Pipeline(chunk_bytes=1 << 20, depth=2)
+    p.run(rk, src, dst)
+    assert np.array_equal(dst.numpy(), oracle.encrypt(key, host, nthreads=4))
+    p.close()
