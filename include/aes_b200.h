@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define AES_B200_ABI_VERSION 1
+#define AES_B200_ABI_VERSION 2   /* 2: AES_VAR_GLOBAL, aes_launch_config.flags, AES_ECAPTURE */
 
 typedef enum {
     AES_OK = 0,
@@ -48,7 +48,8 @@ typedef enum {
     AES_ERANGE = 6,     /* 16*nblocks overflows, or a config value out of range   */
     AES_ENOTDEVICE = 7, /* in/out not device memory of the current device         */
     AES_ECUDA = 8,      /* a CUDA runtime call failed; see aes_last_cuda_error()  */
-    AES_EVARIANT = 9    /* unknown kernel variant / states-per-thread             */
+    AES_EVARIANT = 9,   /* unknown kernel variant / states-per-thread             */
+    AES_ECAPTURE = 10   /* aes_ecb_batch called on a stream under graph capture   */
 } aes_status;
 
 /* Expanded key.  Plain old data, caller-owned, 488 bytes.
@@ -128,15 +129,19 @@ aes_status aes_cbc_decrypt(const aes_round_keys *rk, int nr, const uint8_t *iv, 
  *  keys  : host array of 1..128 round keys (passed by value in the kernel parameters), all
  *          with the same nr (else AES_ENR).
  *  segs  : host array of nsegs descriptors; read during the call only (they are
- *          staged to the device in a stream-ordered allocation freed after the
- *          kernel).  Offsets must be multiples of 16 (AES_EALIGN); a segment's
+ *          copied into a library-owned page-locked staging slot -- a ring of
+ *          slots per device, each reused only after its previous copy has run --
+ *          and from there into a stream-ordered device allocation freed after
+ *          the kernel).  Offsets must be multiples of 16 (AES_EALIGN); a segment's
  *          output must equal or be disjoint from its own input (AES_EOVERLAP);
  *          outputs of DIFFERENT segments must not overlap other segments'
  *          inputs or outputs (not checked: O(n^2)); empty segments are allowed.
  *  in_base/out_base : device pointers of the current device, 16-byte aligned.
- * Asynchronous on `stream`.  Errors: AES_ENULL, AES_ERANGE (nkeys not in 1..128, key_index
+ * Asynchronous on `stream`; NOT capturable into a CUDA graph (the staged
+ * descriptors live in a reused host slot): a stream under capture returns
+ * AES_ECAPTURE.  Errors: AES_ENULL, AES_ERANGE (nkeys not in 1..128, key_index
  * out of range, size overflow), AES_ENR, AES_EALIGN, AES_EOVERLAP,
- * AES_ENOTDEVICE, AES_ECUDA. */
+ * AES_ENOTDEVICE, AES_ECUDA, AES_ECAPTURE. */
 typedef struct {
     uint64_t in_offset;   /* bytes from in_base  */
     uint64_t out_offset;  /* bytes from out_base */
@@ -161,26 +166,50 @@ aes_status aes_ecb_batch(const aes_round_keys *keys, int nkeys, int decrypt, con
  *                       in a 2-stage ring per warp.  states_per_thread must be 1.
  *  AES_VAR_SMEM_ROT   : ONE lane-replicated table (Te0 / Td0) and the other three
  *                       as funnel-shift rotations (Eqs 23-25 are byte rotations
- *                       of Eq 22): 64 KiB of shared memory instead of 128/192. */
+ *                       of Eq 22): 64 KiB of shared memory instead of 128/192.
+ *  AES_VAR_GLOBAL     : tables left in global memory, read through the
+ *                       read-only L1 path (__ldg); no shared memory. */
 typedef enum {
     AES_VAR_DEFAULT = 0,
     AES_VAR_SMEM_REPL = 1,
     AES_VAR_SMEM_PLAIN = 2,
     AES_VAR_CONST = 3,
     AES_VAR_SMEM_REPL_TMA = 4,
-    AES_VAR_SMEM_ROT = 5
+    AES_VAR_SMEM_ROT = 5,
+    AES_VAR_GLOBAL = 6
 } aes_variant;
+
+/* aes_launch_config.flags (bitwise OR):
+ *  AES_LAUNCH_TRUSTED_PTRS : skip the two cudaPointerGetAttributes queries
+ *                            that classify in/out (AES_ENOTDEVICE); for callers
+ *                            that already know both are device memory of the
+ *                            current device (e.g. a prepared call that checked
+ *                            them once).  A host pointer passed with this flag
+ *                            faults in the kernel instead of being rejected.
+ *                            Alignment/overlap/size checks still run.
+ *  AES_LAUNCH_NO_PDL       : launch without programmatic dependent launch.  By
+ *                            default every kernel is launched with the PDL
+ *                            attribute: it starts (and fills its shared-memory
+ *                            tables) while the previous kernel on the stream
+ *                            drains, and waits for that kernel (griddepcontrol
+ *                            .wait) before touching in/out.  Results are
+ *                            identical either way. */
+#define AES_LAUNCH_TRUSTED_PTRS 1
+#define AES_LAUNCH_NO_PDL 2
 
 typedef struct {
     int32_t variant;           /* aes_variant                                      */
     int32_t states_per_thread; /* 0 = default; else 1, 2 or 4 (granularity, 8(a) A10) */
     int32_t grid;              /* 0 = persistent default (SMs x resident CTAs)     */
-    int32_t reserved;
+    int32_t flags;             /* AES_LAUNCH_* bits; 0 = checked pointers + PDL    */
 } aes_launch_config;
 
 /* Same contract as aes_ecb_encrypt/decrypt (decrypt = 0/1) with an explicit
  * variant; cfg may be NULL (= defaults).  AES_EVARIANT for an unknown variant
- * or states_per_thread value, AES_ERANGE for a negative grid. */
+ * or states_per_thread value, AES_ERANGE for a negative grid or unknown flag
+ * bits.  Work split (every variant): whole trips of grid x 1024 x S blocks
+ * grid-stride, the remainder (all of a small message) as one contiguous
+ * warp-aligned chunk per CTA, so every launched CTA has work. */
 aes_status aes_ecb_launch(const aes_round_keys *rk, int nr, int decrypt, const void *in,
                           void *out, uint64_t nblocks, void *stream,
                           const aes_launch_config *cfg);

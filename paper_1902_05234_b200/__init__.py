@@ -15,13 +15,15 @@ from __future__ import annotations
 import ctypes
 
 from . import _native
-from ._native import (AES_VAR_CONST, AES_VAR_DEFAULT, AES_VAR_SMEM_PLAIN, AES_VAR_SMEM_REPL, AES_VAR_SMEM_REPL_TMA, AES_VAR_SMEM_ROT,
-                      aes_launch_config, aes_round_keys, status_string)
+from ._native import (AES_LAUNCH_NO_PDL, AES_LAUNCH_TRUSTED_PTRS, AES_VAR_CONST, AES_VAR_DEFAULT, AES_VAR_GLOBAL,
+                      AES_VAR_SMEM_PLAIN, AES_VAR_SMEM_REPL, AES_VAR_SMEM_REPL_TMA, AES_VAR_SMEM_ROT, aes_launch_config,
+                      aes_round_keys, status_string)
 
 __all__ = ["RoundKeys", "expand_key", "ecb_encrypt", "ecb_decrypt", "ecb", "ecb_batch", "ecb_batch_offsets", "KeySet", "ctr_xcrypt", "cbc_decrypt",
            "ecb_trace", "Pipeline",
            "lds_gather", "AesError", "AES_VAR_DEFAULT", "AES_VAR_SMEM_REPL", "AES_VAR_SMEM_PLAIN",
-           "AES_VAR_CONST", "AES_VAR_SMEM_REPL_TMA", "AES_VAR_SMEM_ROT", "abi_version"]
+           "AES_VAR_CONST", "AES_VAR_SMEM_REPL_TMA", "AES_VAR_SMEM_ROT", "AES_VAR_GLOBAL", "AES_LAUNCH_TRUSTED_PTRS",
+           "AES_LAUNCH_NO_PDL", "abi_version", "prepare_ecb", "EcbCall"]
 
 
 class AesError(RuntimeError):
@@ -41,10 +43,11 @@ def _check(code: int, what: str):
 class RoundKeys:
     """Expanded key (aes_round_keys): ek, dk (equivalent inverse), nr, keybits."""
 
-    __slots__ = ("c",)
+    __slots__ = ("c", "c_ref")
 
     def __init__(self, c: aes_round_keys):
         self.c = c
+        self.c_ref = ctypes.byref(c)   # built once: byref() per call costs ~0.3 us
 
     @property
     def nr(self) -> int:
@@ -105,6 +108,9 @@ def _on_device(dev):
 
 def _check_tensor(x, name):
     import torch
+    if type(x) is torch.Tensor and x.dtype is torch.uint8 and x.is_cuda and x.is_contiguous() \
+            and not x.numel() & 15:
+        return                                  # the common case: one combined test
     if not isinstance(x, torch.Tensor):
         raise TypeError(f"{name} must be a torch tensor")
     if not x.is_cuda:
@@ -118,28 +124,93 @@ def _check_tensor(x, name):
 
 
 def ecb(rk: RoundKeys, x, decrypt: bool, out=None, variant: int = AES_VAR_DEFAULT,
-        states_per_thread: int = 0, grid: int = 0, stream=None):
-    """ECB over a device buffer; ``out`` may be ``x`` (in place) or None (new tensor)."""
+        states_per_thread: int = 0, grid: int = 0, stream=None, flags: int = 0):
+    """ECB over a device buffer; ``out`` may be ``x`` (in place) or None (new tensor).
+    ``flags``: AES_LAUNCH_* bits (aes_launch_config.flags)."""
     import torch
     _check_tensor(x, "x")
     if out is None:
         out = torch.empty_like(x)
-    else:
+    elif out is not x:
         _check_tensor(out, "out")
         if out.numel() != x.numel():
             raise ValueError("out must have the same size as x")
-    n = x.numel() // 16
+    n = x.numel() >> 4
     with _on_device(x.device):
         sp = stream.cuda_stream if stream is not None else _raw_stream(x.device.index)
-        if variant == AES_VAR_DEFAULT and not states_per_thread and not grid:
+        if variant == AES_VAR_DEFAULT and not states_per_thread and not grid and not flags:
             fn = _native.lib.aes_ecb_decrypt if decrypt else _native.lib.aes_ecb_encrypt
-            code = fn(ctypes.byref(rk.c), rk.nr, x.data_ptr(), out.data_ptr(), n, sp)
+            code = fn(rk.c_ref, rk.nr, x.data_ptr(), out.data_ptr(), n, sp)
         else:
-            cfg = aes_launch_config(variant, states_per_thread, grid, 0)
-            code = _native.lib.aes_ecb_launch(ctypes.byref(rk.c), rk.nr, int(bool(decrypt)),
+            cfg = aes_launch_config(variant, states_per_thread, grid, flags)
+            code = _native.lib.aes_ecb_launch(rk.c_ref, rk.nr, int(bool(decrypt)),
                                               x.data_ptr(), out.data_ptr(), n, sp, ctypes.byref(cfg))
-    _check(code, "aes_ecb_decrypt" if decrypt else "aes_ecb_encrypt")
+    if code:
+        _check(code, "aes_ecb_decrypt" if decrypt else "aes_ecb_encrypt")
     return out
+
+
+class EcbCall:
+    """A prepared ECB call over fixed device buffers -- the per-call fast path.
+
+    Everything that does not change between calls is decided once here: the
+    tensors are validated (contiguous uint8 CUDA memory of one device, sizes,
+    in == out or disjoint), the ctypes arguments are packed, and the launch
+    carries AES_LAUNCH_TRUSTED_PTRS so the library skips its per-call
+    cudaPointerGetAttributes queries (torch already guarantees device memory).
+    Each ``call()`` (or ``__call__``) then costs one raw-stream query plus the
+    C ABI call: aes_ecb_launch on torch's current stream (or ``stream``).
+    The tensors must stay alive (and in place) while the object is used."""
+
+    __slots__ = ("_fn", "_args", "_dev", "x", "out")
+
+    def __init__(self, rk: RoundKeys, x, out=None, decrypt: bool = False, variant: int = AES_VAR_DEFAULT,
+                 states_per_thread: int = 0, grid: int = 0, flags: int = 0):
+        import torch
+        _check_tensor(x, "x")
+        if out is None:
+            out = torch.empty_like(x)
+        _check_tensor(out, "out")
+        if out.numel() != x.numel() or out.device != x.device:
+            raise ValueError("out must have the size and device of x")
+        self.x, self.out = x, out
+        self._dev = x.device.index
+        cfg = aes_launch_config(variant, states_per_thread, grid, flags | AES_LAUNCH_TRUSTED_PTRS)
+        self._fn = _native.lib.aes_ecb_launch
+        # the keys are copied into the object: later changes to rk do not leak in
+        kc = aes_round_keys.from_buffer_copy(rk.c)
+        self._args = [ctypes.byref(kc), rk.nr, int(bool(decrypt)), ctypes.c_void_p(x.data_ptr()),
+                      ctypes.c_void_p(out.data_ptr()), x.numel() >> 4, None, ctypes.byref(cfg), kc, cfg]
+        # what the library would check per call, checked once: alignment,
+        # overlap (in == out allowed), then variant/flags/keys via a zero-block call
+        pi, po, nb = x.data_ptr(), out.data_ptr(), x.numel()
+        if (pi | po) & 15:
+            raise AesError(_native.AES_EALIGN, "aes_ecb_launch")
+        if pi != po and pi < po + nb and po < pi + nb:
+            raise AesError(_native.AES_EOVERLAP, "aes_ecb_launch")
+        code = self._fn(*self._args[:5], 0, None, self._args[7])
+        if code:
+            _check(code, "aes_ecb_launch")
+
+    def __call__(self, stream=None):
+        import torch
+        a = self._args
+        dev = self._dev
+        if torch.cuda.current_device() != dev:
+            with torch.cuda.device(dev):
+                return self.__call__(stream)
+        code = self._fn(a[0], a[1], a[2], a[3], a[4], a[5],
+                        stream.cuda_stream if stream is not None else _raw_stream(dev), a[7])
+        if code:
+            _check(code, "aes_ecb_launch")
+        return self.out
+
+    call = __call__
+
+
+def prepare_ecb(rk: RoundKeys, x, out=None, decrypt: bool = False, **kw) -> EcbCall:
+    """EcbCall(rk, x, out, decrypt): the per-call fast path over fixed buffers."""
+    return EcbCall(rk, x, out, decrypt, **kw)
 
 
 def ecb_encrypt(rk: RoundKeys, x, out=None, **kw):
@@ -170,7 +241,7 @@ def ctr_xcrypt(rk: RoundKeys, iv: bytes, x, out=None, block_offset: int = 0, str
     out = _prep_out(x, out)
     with _on_device(x.device):
         sp = stream.cuda_stream if stream is not None else _raw_stream(x.device.index)
-        code = _native.lib.aes_ctr_xcrypt(ctypes.byref(rk.c), rk.nr, iv, block_offset & (2**64 - 1),
+        code = _native.lib.aes_ctr_xcrypt(rk.c_ref, rk.nr, iv, block_offset & (2**64 - 1),
                                           x.data_ptr(), out.data_ptr(), x.numel() // 16, sp)
     _check(code, "aes_ctr_xcrypt")
     return out
@@ -185,7 +256,7 @@ def cbc_decrypt(rk: RoundKeys, iv: bytes, x, out=None, stream=None):
     out = _prep_out(x, out)
     with _on_device(x.device):
         sp = stream.cuda_stream if stream is not None else _raw_stream(x.device.index)
-        code = _native.lib.aes_cbc_decrypt(ctypes.byref(rk.c), rk.nr, iv, x.data_ptr(), out.data_ptr(),
+        code = _native.lib.aes_cbc_decrypt(rk.c_ref, rk.nr, iv, x.data_ptr(), out.data_ptr(),
                                            x.numel() // 16, sp)
     _check(code, "aes_cbc_decrypt")
     return out
@@ -267,7 +338,7 @@ def ecb_trace(rk: RoundKeys, x, rounds: int, decrypt: bool = False, out=None):
     """aes_ecb_trace: state after ARK(0) + `rounds` rounds (round-by-round parity pin)."""
     out = _prep_out(x, out)
     with _on_device(x.device):
-        code = _native.lib.aes_ecb_trace(ctypes.byref(rk.c), rk.nr, int(bool(decrypt)), int(rounds), x.data_ptr(),
+        code = _native.lib.aes_ecb_trace(rk.c_ref, rk.nr, int(bool(decrypt)), int(rounds), x.data_ptr(),
                                          out.data_ptr(), x.numel() // 16, _raw_stream(x.device.index))
     _check(code, "aes_ecb_trace")
     return out
@@ -308,7 +379,7 @@ class Pipeline:
         pd, nd = self._ptr_len(dst)
         if ns != nd or ns % 16:
             raise ValueError("src/dst must have equal sizes, a multiple of 16")
-        _check(_native.lib.aes_pipeline_run(self.h, ctypes.byref(rk.c), rk.nr, int(bool(decrypt)),
+        _check(_native.lib.aes_pipeline_run(self.h, rk.c_ref, rk.nr, int(bool(decrypt)),
                                             ctypes.c_void_p(ps), ctypes.c_void_p(pd), ns // 16),
                "aes_pipeline_run")
         return dst

@@ -13,9 +13,11 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libaes_b200.so")
 
 AES_OK, AES_EKEYBITS, AES_ENR, AES_ENULL, AES_EALIGN, AES_EOVERLAP, AES_ERANGE, \
-    AES_ENOTDEVICE, AES_ECUDA, AES_EVARIANT = range(10)
+    AES_ENOTDEVICE, AES_ECUDA, AES_EVARIANT, AES_ECAPTURE = range(11)
 
-AES_VAR_DEFAULT, AES_VAR_SMEM_REPL, AES_VAR_SMEM_PLAIN, AES_VAR_CONST, AES_VAR_SMEM_REPL_TMA, AES_VAR_SMEM_ROT = range(6)
+AES_VAR_DEFAULT, AES_VAR_SMEM_REPL, AES_VAR_SMEM_PLAIN, AES_VAR_CONST, AES_VAR_SMEM_REPL_TMA, AES_VAR_SMEM_ROT, \
+    AES_VAR_GLOBAL = range(7)
+AES_LAUNCH_TRUSTED_PTRS, AES_LAUNCH_NO_PDL = 1, 2
 
 # every symbol include/aes_b200.h declares
 EXPORTS = ("aes_expand_key", "aes_ecb_encrypt", "aes_ecb_decrypt", "aes_ecb_launch",
@@ -35,7 +37,7 @@ class aes_segment(ctypes.Structure):
 
 class aes_launch_config(ctypes.Structure):
     _fields_ = [("variant", ctypes.c_int32), ("states_per_thread", ctypes.c_int32),
-                ("grid", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("grid", ctypes.c_int32), ("flags", ctypes.c_int32)]
 
 
 def _load():

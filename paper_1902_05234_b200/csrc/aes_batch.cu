@@ -52,7 +52,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     batch_kernel(const char* __restrict__ in_base, char* __restrict__ out_base, const BatchSeg* __restrict__ segs,
                  uint32_t nsegs, uint64_t total, const __grid_constant__ BatchKeys<KCAP> keys) {
     extern __shared__ __align__(16) uint32_t smem[];
+    pdl_launch_dependents();
     const Tab<V_REPL> tb = Tab<V_REPL>::template setup<DEC>(smem);   // ends with __syncthreads
+    pdl_wait();
     const uint64_t per = (total + gridDim.x - 1) / gridDim.x;
     const uint64_t c0 = per * blockIdx.x, c1 = c0 + per < total ? c0 + per : total;
     const uint32_t lane = threadIdx.x & 31;
@@ -173,9 +175,13 @@ extern "C" aes_status aes_ecb_batch(const aes_round_keys* keys, int nkeys, int d
     }
     if (total == 0) return AES_OK;
     int dev = 0, occ = 1, nsm = 148;
+    cudaStream_t cs0 = (cudaStream_t)stream;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e);
     aes_status st;
+    cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+    if ((e = cudaStreamIsCapturing(cs0, &cap_st)) != cudaSuccess) return cuda_fail(e);
+    if (cap_st != cudaStreamCaptureStatusNone) return AES_ECAPTURE;   // staged descriptors are not replayable
     if ((st = check_device_ptr(in_base, dev))) return st;
     if (out_base != in_base && (st = check_device_ptr(out_base, dev))) return st;
     const int kcap = nkeys <= 16 ? 16 : nkeys <= 64 ? 64 : kBatchMaxKeys;   // parameter bytes scale with the tier
@@ -212,8 +218,9 @@ extern "C" aes_status aes_ecb_batch(const aes_round_keys* keys, int nkeys, int d
     void* args[] = {(void*)&pin, (void*)&pout, (void*)&dsegs, (void*)&nsegs, (void*)&total,
                     kcap == 16 ? (void*)&ksmall : kcap == 64 ? (void*)&kmid : (void*)&kbig};
     uint64_t want = (total + 31) / 32, cap = (uint64_t)nsm * occ;
-    e = cudaLaunchKernel(f, dim3((unsigned)(want < cap ? want : cap)), dim3(kThreads), args, smem, cs);
+    // no PDL: the kernel's predecessor on the stream is the descriptor copy
+    st = launch_kernel(ki, (unsigned)(want < cap ? want : cap), args, cs, false);
     cudaError_t e2 = cudaFreeAsync(d, cs);
-    if (e != cudaSuccess) return cuda_fail(e);
+    if (st) return st;
     return e2 == cudaSuccess ? AES_OK : cuda_fail(e2);
 }

@@ -79,7 +79,45 @@ constexpr size_t kSmemReplDec = 2 * kRegion + 255 * 256 + 128;
 constexpr size_t kSmemPlain = (4 * 256 + 256) * 4;
 constexpr size_t kSmemRot = 255 * 256 + 256;   // one replicated table (+ Si4 for decryption) in a 64 KiB region
 
-enum { V_REPL = 1, V_PLAIN = 2, V_CONST = 3, V_REPL_TMA = 4, V_ROT = 5 };
+enum { V_REPL = 1, V_PLAIN = 2, V_CONST = 3, V_REPL_TMA = 4, V_ROT = 5, V_GLOBAL = 6 };
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL).  Every kernel lets the next kernel of
+// its stream be scheduled at once (launch_dependents) and waits for the
+// previous one only after its own table fill (pdl_wait), so back-to-back
+// launches overlap the next launch's latency and 128-192 KiB prologue with
+// this one's tail.  Both are no-ops when the launch carries no PDL attribute.
+// All reads and writes of mutable global memory come after pdl_wait (the
+// table fill before it reads only the immutable g_tab image).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// ---------------------------------------------------------------------------
+// Work split of n blocks over the grid (A10).  Whole trips of TS = SPT * grid
+// threads are walked grid-stride (each warp access = 512 contiguous bytes, one
+// moving DRAM window).  The remainder rem < TS -- the whole message when it is
+// small -- is cut into per-CTA contiguous, warp-aligned chunks of
+// c = ceil(rem / grid) rounded up to 32 blocks (c <= SPT * blockDim), so every
+// CTA that paid its table fill gets work instead of the first rem/1024 CTAs
+// taking all of it.
+// ---------------------------------------------------------------------------
+struct Split {
+    uint64_t full;    // blocks [0, full) are walked grid-stride with stride TS
+    uint64_t tbase;   // this CTA's tail chunk starts at tbase ...
+    uint32_t tlen;    // ... and holds tlen blocks (0 <= tlen <= c)
+};
+
+__device__ __forceinline__ Split split_work(uint64_t n, uint64_t TS) {
+    Split sp;
+    sp.full = n - n % TS;
+    const uint64_t rem = n - sp.full;
+    const uint64_t c = ((rem + gridDim.x - 1) / gridDim.x + 31) & ~31ull;
+    const uint64_t b0 = (uint64_t)blockIdx.x * c;
+    sp.tbase = sp.full + b0;
+    sp.tlen = b0 >= rem ? 0u : (uint32_t)(rem - b0 < c ? rem - b0 : c);
+    return sp;
+}
 
 // ---------------------------------------------------------------------------
 // Table access policies: t(i, s, k) = T_i[byte k of s];  si(s, k) = Si4[byte k of s]
@@ -212,6 +250,25 @@ struct Tab<V_CONST> {
     __device__ __forceinline__ static Tab setup(uint32_t*) {
         Tab tb;
         tb.dec = DEC;
+        return tb;
+    }
+};
+
+// Tables left in global memory and read through the read-only L1 path
+// (__ldg, LDG.E.CONSTANT): the fourth placement of the NEXT-2 ablation.  The
+// 4 KiB (+1 KiB Si4) image stays L1-resident; a warp's 32 divergent addresses
+// cost one L1 tag lookup per distinct 128-byte line.
+template <>
+struct Tab<V_GLOBAL> {
+    const uint32_t* t4;
+    __device__ __forceinline__ uint32_t t(int i, uint32_t s, int k) const {
+        return __ldg(t4 + i * 256 + ((s >> (8 * k)) & 255));
+    }
+    __device__ __forceinline__ uint32_t si(uint32_t s, int k) const { return __ldg(g_tab.si4 + ((s >> (8 * k)) & 255)); }
+    template <bool DEC>
+    __device__ __forceinline__ static Tab setup(uint32_t*) {
+        Tab tb;
+        tb.t4 = DEC ? &g_tab.td[0][0] : &g_tab.te[0][0];
         return tb;
     }
 };

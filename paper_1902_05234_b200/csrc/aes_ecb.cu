@@ -71,14 +71,19 @@ template <int NR, bool DEC, int V, int SPT, int MODE>
 __device__ __forceinline__ void aes_body(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n,
                                          const RK& rk, const ModeP& mp) {
     extern __shared__ __align__(16) uint32_t smem[];
+    pdl_launch_dependents();
     const Tab<V> tb = Tab<V>::template setup<DEC>(smem);   // A4
+    pdl_wait();
     const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += SPT * T) {
+    const Split sp = split_work(n, SPT * T);
+    // one trip: SPT states at i, i + stride, ..., those with their okmask bit set
+    auto trip = [&](uint64_t i, uint64_t stride, uint32_t okmask) {
         uint4 v[SPT], w[SPT];
 #pragma unroll
         for (int k = 0; k < SPT; k++) {
-            const uint64_t j = i + k * T;
-            if (j < n) {                                                   // A5
+            v[k] = w[k] = make_uint4(0, 0, 0, 0);
+            const uint64_t j = i + k * stride;
+            if (okmask >> k & 1) {                                         // A5
                 if (MODE == M_ECB) v[k] = __ldcs(in + j);
                 if (MODE == M_CTR) { v[k] = counter_block(mp, j); w[k] = __ldcs(in + j); }
                 if (MODE == M_CBCD) {
@@ -90,28 +95,48 @@ __device__ __forceinline__ void aes_body(const uint4* __restrict__ in, uint4* __
 #pragma unroll
         for (int k = 0; k < SPT; k++) v[k] = cipher_block<NR, DEC>(tb, v[k], rk);   // A6-A8
 #pragma unroll
-        for (int k = 0; k < SPT; k++) {
-            const uint64_t j = i + k * T;
-            if (j < n) __stcs(out + j, MODE == M_ECB ? v[k] : xor4(v[k], w[k]));   // A9
-        }
-    }
+        for (int k = 0; k < SPT; k++)
+            if (okmask >> k & 1) __stcs(out + i + k * stride, MODE == M_ECB ? v[k] : xor4(v[k], w[k]));   // A9
+    };
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sp.full; i += SPT * T)
+        trip(i, T, (1u << SPT) - 1);
+    // tail: this CTA's contiguous chunk, blockDim-strided
+    uint32_t okmask = 0;
+#pragma unroll
+    for (int k = 0; k < SPT; k++) okmask |= (threadIdx.x + k * blockDim.x < sp.tlen ? 1u : 0u) << k;
+    if (okmask) trip(sp.tbase + threadIdx.x, blockDim.x, okmask);
 }
 
 // ECB with the next trip's state load issued before the current trip's rounds
 // (software prefetch across loop iterations; the compiler does not hoist it).
+// Sequence of this thread's blocks: gid, gid + T, ... (< full), then its tail block.
 template <int NR, bool DEC, int V>
 __device__ __forceinline__ void ecb_prefetch_body(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n,
                                                   const RK& rk) {
     extern __shared__ __align__(16) uint32_t smem[];
+    pdl_launch_dependents();
     const Tab<V> tb = Tab<V>::template setup<DEC>(smem);
+    pdl_wait();
     const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    const Split sp = split_work(n, T);
+    const uint64_t tail = sp.tbase + threadIdx.x;
+    const bool has_tail = threadIdx.x < sp.tlen;
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool valid = true;
+    if (i >= sp.full) { i = tail; valid = has_tail; }
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (i < n) v = __ldcs(in + i);
-    for (; i < n; i += T) {
+    if (valid) v = __ldcs(in + i);
+    while (valid) {
         const uint4 cur = v;
-        if (i + T < n) v = __ldcs(in + i + T);
-        __stcs(out + i, cipher_block<NR, DEC>(tb, cur, rk));
+        const uint64_t ci = i;
+        if (i < sp.full) {
+            i += T;
+            if (i >= sp.full) { i = tail; valid = has_tail; }
+        } else {
+            valid = false;
+        }
+        if (valid) v = __ldcs(in + i);
+        __stcs(out + ci, cipher_block<NR, DEC>(tb, cur, rk));
     }
 }
 
@@ -168,7 +193,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     ctr_cached_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n,
                       const __grid_constant__ RK rk, const __grid_constant__ ModeP mp) {
     extern __shared__ __align__(16) uint32_t smem[];
+    pdl_launch_dependents();
     const Tab<V_REPL> tb = Tab<V_REPL>::template setup<false>(smem);
+    pdl_wait();
     // Warp-private table of group constants for the warp's next 16 trips x
     // (the <= 2 groups its 32 consecutive blocks touch): 32 entries x 8 words,
     // filled by the 32 lanes in parallel -- 27 LDS instructions per 16 trips
@@ -224,7 +251,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     trace_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n, const __grid_constant__ RK rk,
                  int rounds) {
     extern __shared__ __align__(16) uint32_t smem[];
+    pdl_launch_dependents();
     const Tab<V_REPL> tb = Tab<V_REPL>::template setup<DEC>(smem);
+    pdl_wait();
     const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += T) {
         uint4 v = in[i];
@@ -285,7 +314,9 @@ template <int NR, bool DEC>
 __global__ void __launch_bounds__(kThreads, 1)
     ecb_tma_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n, const __grid_constant__ RK rk) {
     extern __shared__ __align__(16) uint32_t smem[];
+    pdl_launch_dependents();
     const Tab<V_REPL> tb = Tab<V_REPL>::template setup<DEC>(smem);
+    pdl_wait();
     const size_t tab_bytes = DEC ? kSmemReplDec : kSmemReplEnc;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     char* ring = reinterpret_cast<char*>(smem) + tab_bytes + warp * kTmaStages * kTmaTileBytes;
@@ -351,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int NR, bool DEC, int V, int SPT>
 KernelInfo kinfo() {
-    size_t sm = V == V_REPL ? (DEC ? kSmemReplDec : kSmemReplEnc) : V == V_PLAIN ? kSmemPlain : V == V_ROT ? kSmemRot : 0;
+    size_t sm = V == V_REPL ? (DEC ? kSmemReplDec : kSmemReplEnc) : V == V_PLAIN ? kSmemPlain : V == V_ROT ? kSmemRot : 0;   // CONST, GLOBAL: none
     return {reinterpret_cast<const void*>(&ecb_kernel<NR, DEC, V, SPT>), sm};
 }
 
@@ -370,6 +401,7 @@ KernelInfo pick_spt(int v, int spt) {
         if (v == V_PLAIN) return kinfo<NR, DEC, V_PLAIN, 1>();
         if (v == V_ROT) return kinfo<NR, DEC, V_ROT, 1>();
         if (v == V_CONST) return kinfo<NR, DEC, V_CONST, 1>();
+        if (v == V_GLOBAL) return kinfo<NR, DEC, V_GLOBAL, 1>();
     }
     return {nullptr, 0};
 }
@@ -413,9 +445,11 @@ aes_status launch(const aes_round_keys* rk, int nr, int decrypt, const void* in,
     int variant = cfg ? cfg->variant : AES_VAR_DEFAULT;
     int spt = cfg ? cfg->states_per_thread : 0;
     int grid_req = cfg ? cfg->grid : 0;
+    const int flags = cfg ? cfg->flags : 0;
     if (variant == AES_VAR_DEFAULT) variant = V_REPL;   // measured best
     if (spt == 0) spt = 1;                              // S = 1, 2, 4 measure within 1 %
-    if (grid_req < 0) return AES_ERANGE;
+    if (grid_req < 0 || (flags & ~(AES_LAUNCH_TRUSTED_PTRS | AES_LAUNCH_NO_PDL))) return AES_ERANGE;
+    if (flags & AES_LAUNCH_TRUSTED_PTRS) check_ptrs = false;
     KernelInfo ki = mode == M_ECB ? pick(nr, decrypt != 0, variant, spt) : pick_mode(nr, mode);
     if (mode != M_ECB) spt = 1;
     if (!ki.fn) return AES_EVARIANT;
@@ -431,9 +465,10 @@ aes_status launch(const aes_round_keys* rk, int nr, int decrypt, const void* in,
     }
     int occ = 1, nsm = 148;
     if ((st = resident_ctas(dev, ki, &occ, &nsm))) return st;
-    // Spread small and medium buffers over every SM (at least one full warp of
-    // states per CTA) instead of packing 1024 states into each CTA: the per-CTA
-    // table fill is ~0.5 us, the lookups are what must be parallel.
+    // Persistent grid (SMs x resident CTAs), or fewer CTAs when the message is
+    // small: every CTA gets >= 32 blocks (one full warp), because each one
+    // pays a 128-192 KiB table fill.  The kernels split the remainder of whole
+    // trips into one contiguous chunk per CTA (split_work), so all of them work.
     uint64_t per_cta = 32ull * spt;
     uint64_t want = (nblocks + per_cta - 1) / per_cta;
     uint64_t cap = grid_req ? (uint64_t)grid_req : (uint64_t)nsm * occ;
@@ -444,9 +479,7 @@ aes_status launch(const aes_round_keys* rk, int nr, int decrypt, const void* in,
     uint4* pout = static_cast<uint4*>(out);
     ModeP m = mp ? *mp : ModeP{};
     void* args[] = {(void*)&pin, (void*)&pout, (void*)&nblocks, (void*)&k, (void*)&m};
-    e = cudaLaunchKernel(ki.fn, dim3(grid), dim3(kThreads), args, ki.smem, stream);
-    if (e != cudaSuccess) return cuda_fail(e);
-    return AES_OK;
+    return launch_kernel(ki, grid, args, stream, !(flags & AES_LAUNCH_NO_PDL));
 }
 
 aes_status launch_ecb(const aes_round_keys* rk, int nr, int decrypt, const void* in, void* out, uint64_t nblocks,
@@ -526,9 +559,7 @@ aes_status aes_ecb_trace(const aes_round_keys* rk, int nr, int decrypt, int roun
     const uint4* pin = static_cast<const uint4*>(in);
     uint4* pout = static_cast<uint4*>(out);
     void* args[] = {(void*)&pin, (void*)&pout, (void*)&nblocks, (void*)&k, (void*)&rounds};
-    e = cudaLaunchKernel(f, dim3((unsigned)(want < cap ? want : cap)), dim3(kThreads), args, ki.smem,
-                         (cudaStream_t)stream);
-    return e == cudaSuccess ? AES_OK : cuda_fail(e);
+    return launch_kernel(ki, (unsigned)(want < cap ? want : cap), args, (cudaStream_t)stream, true);
 }
 
 aes_status aes_mb_lds_gather(void* sink, int grid, int iters, void* stream) {

@@ -21,8 +21,9 @@ constexpr int kThreads = 1024;   // every kernel runs 1024-thread CTAs (one per 
 
 aes_status cuda_fail(cudaError_t e);                       // records e for aes_last_cuda_error()
 aes_status resident_ctas(int dev, const KernelInfo& ki, int* occ, int* nsm);   // sets smem attr once
+aes_status launch_kernel(const KernelInfo& ki, unsigned grid, void** args, cudaStream_t stream, bool pdl);
 aes_status desc_pool(int dev, cudaMemPool_t* out);         // stream-ordered pool for descriptors
-aes_status stage_h2d(int dev, void* dst, const void* src, size_t bytes, cudaStream_t s);   // pinned async H2D
+aes_status stage_h2d(int dev, void* dst, const void* src, size_t bytes, cudaStream_t s);   // pinned ring, async H2D
 aes_status validate_keys(const aes_round_keys* rk, int nr);
 aes_status validate_buffers(const void* in, const void* out, uint64_t nblocks);
 aes_status check_device_ptr(const void* p, int dev);

@@ -1,5 +1,6 @@
 // aes_runtime.cu -- host runtime of libaes_b200.so: CUDA error capture,
-// the per-device launch-attribute cache, the descriptor memory pool, argument
+// the per-device launch-attribute cache, the PDL launch helper, the descriptor
+// memory pool and staging ring, argument
 // validation (everything decided before a launch, include/aes_b200.h "Errors"),
 // status strings.
 #include <cuda_runtime.h>
@@ -7,6 +8,8 @@
 #include <cstdint>
 #include <cstring>
 #include <mutex>
+#include <shared_mutex>
+#include <unordered_map>
 
 #include "aes_b200.h"
 #include "aes_host.h"
@@ -20,18 +23,24 @@ aes_status cuda_fail(cudaError_t e) {
     return AES_ECUDA;
 }
 
-// Per-(device, kernel) resident-CTA count; set the dynamic-smem attribute once.
-std::mutex g_attr_mu;
-struct AttrEntry {
-    const void* fn;
-    int occ;
-};
-AttrEntry g_attr[kMaxDev][128];
+// Per-(device, kernel) resident-CTA count; the dynamic-smem attribute is set
+// once per (device, kernel) under the write lock, later calls take a shared lock.
+std::shared_mutex g_attr_mu;
+std::unordered_map<const void*, int> g_occ[kMaxDev];
 int g_nsm[kMaxDev];
 
 aes_status resident_ctas(int dev, const KernelInfo& ki, int* occ, int* nsm) {
     if (dev < 0 || dev >= kMaxDev) return AES_ERANGE;
-    std::lock_guard<std::mutex> g(g_attr_mu);
+    {
+        std::shared_lock<std::shared_mutex> rd(g_attr_mu);
+        auto it = g_occ[dev].find(ki.fn);
+        if (it != g_occ[dev].end()) {
+            *occ = it->second;
+            *nsm = g_nsm[dev];
+            return AES_OK;
+        }
+    }
+    std::unique_lock<std::shared_mutex> wr(g_attr_mu);
     if (!g_nsm[dev]) {
         int v = 0;
         cudaError_t e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
@@ -39,22 +48,38 @@ aes_status resident_ctas(int dev, const KernelInfo& ki, int* occ, int* nsm) {
         g_nsm[dev] = v;
     }
     *nsm = g_nsm[dev];
-    int slot = -1;
-    for (int s = 0; s < 128; s++) {
-        if (g_attr[dev][s].fn == ki.fn) { *occ = g_attr[dev][s].occ; return AES_OK; }
-        if (!g_attr[dev][s].fn) { slot = s; break; }
+    auto it = g_occ[dev].find(ki.fn);
+    if (it != g_occ[dev].end()) {
+        *occ = it->second;
+        return AES_OK;
     }
-    if (slot < 0) return AES_ERANGE;
     cudaError_t e = cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ki.smem);
     if (e != cudaSuccess) return cuda_fail(e);
     int o = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ki.fn, kThreads, ki.smem);
     if (e != cudaSuccess) return cuda_fail(e);
     if (o < 1) o = 1;
-    g_attr[dev][slot].fn = ki.fn;
-    g_attr[dev][slot].occ = o;
+    g_occ[dev].emplace(ki.fn, o);
     *occ = o;
     return AES_OK;
+}
+
+// One kernel launch of kThreads-thread CTAs, with the programmatic-dependent-
+// launch attribute unless pdl == false (aes_device.cuh: every kernel fills its
+// tables before griddepcontrol.wait).
+aes_status launch_kernel(const KernelInfo& ki, unsigned grid, void** args, cudaStream_t stream, bool pdl) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = ki.smem;
+    lc.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = pdl ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelExC(&lc, ki.fn, args);
+    return e == cudaSuccess ? AES_OK : cuda_fail(e);
 }
 
 // A library-owned stream-ordered memory pool per device for small per-call
@@ -83,22 +108,50 @@ aes_status desc_pool(int dev, cudaMemPool_t* out) {
     return AES_OK;
 }
 
-// Per-thread, per-device page-locked staging buffer for small host->device
-// descriptor copies: cudaMemcpyAsync from pageable memory is synchronous,
-// from pinned memory it is a plain async DMA.  An event recorded after each
-// copy guards the buffer's reuse by the next call from the same thread.
-struct Staging {
+// Page-locked staging for small host->device descriptor copies (cudaMemcpyAsync
+// from pageable memory is synchronous, from pinned memory a plain async DMA).
+// A process-wide ring of kSlots slots per device: a call takes the next slot
+// whose previous copy has completed (cudaEventQuery, no blocking), and only
+// blocks -- on that slot's own event -- when all kSlots copies are still queued.
+// Slots are released at process exit.
+constexpr int kSlots = 16;
+struct Slot {
     void* host = nullptr;
     size_t cap = 0;
     cudaEvent_t ev = nullptr;
 };
-thread_local Staging t_stage[kMaxDev];
+struct StageRing {
+    std::mutex mu;
+    Slot slot[kSlots];
+    unsigned next = 0;
+    ~StageRing() {
+        for (Slot& s : slot) {
+            if (s.ev) cudaEventDestroy(s.ev);
+            if (s.host) cudaFreeHost(s.host);
+        }
+    }
+};
+StageRing g_stage[kMaxDev];
 
 aes_status stage_h2d(int dev, void* dst, const void* src, size_t bytes, cudaStream_t s) {
     if (dev < 0 || dev >= kMaxDev) return AES_ERANGE;
-    Staging& st = t_stage[dev];
+    StageRing& r = g_stage[dev];
+    std::lock_guard<std::mutex> g(r.mu);
     cudaError_t e;
-    if (st.ev && (e = cudaEventSynchronize(st.ev)) != cudaSuccess) return cuda_fail(e);
+    int pick = -1;
+    for (int k = 0; k < kSlots && pick < 0; k++) {
+        const int c = (int)((r.next + k) % kSlots);
+        if (!r.slot[c].ev) { pick = c; break; }
+        e = cudaEventQuery(r.slot[c].ev);
+        if (e == cudaSuccess) pick = c;
+        else if (e != cudaErrorNotReady) return cuda_fail(e);
+    }
+    if (pick < 0) {   // every slot's copy still queued: wait for the oldest
+        pick = (int)(r.next % kSlots);
+        if ((e = cudaEventSynchronize(r.slot[pick].ev)) != cudaSuccess) return cuda_fail(e);
+    }
+    r.next = (unsigned)pick + 1;
+    Slot& st = r.slot[pick];
     if (st.cap < bytes) {
         if (st.host) cudaFreeHost(st.host);
         st.host = nullptr;
@@ -159,6 +212,7 @@ const char* aes_status_string(aes_status s) {
         case AES_ENOTDEVICE: return "AES_ENOTDEVICE: buffer is not device memory of the current device";
         case AES_ECUDA: return "AES_ECUDA: CUDA runtime error (see aes_last_cuda_error)";
         case AES_EVARIANT: return "AES_EVARIANT: unknown kernel variant or states_per_thread";
+        case AES_ECAPTURE: return "AES_ECAPTURE: aes_ecb_batch cannot be captured into a CUDA graph";
     }
     return "AES_?: unknown status";
 }

@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     lib = ctypes.CDLL(_native.LIB_PATH)
     for name in declared:
         assert hasattr(lib, name), name
-    assert _native.lib.aes_abi_version() == 1
+    assert _native.lib.aes_abi_version() == 2
 
 
 def test_library_is_sm100a_and_has_no_oracle_symbols():
@@ -123,6 +123,11 @@ def test_validation_errors_before_any_cuda_call():
     assert _call(rk, 10, A, A, 4, cfg=cfg) == _native.AES_EVARIANT
     cfg = _native.aes_launch_config(_native.AES_VAR_SMEM_REPL, 1, -1, 0)
     assert _call(rk, 10, A, A, 4, cfg=cfg) == _native.AES_ERANGE
+    for bad_flags in (4, 8, -1):                               # unknown aes_launch_config.flags bits
+        cfg = _native.aes_launch_config(_native.AES_VAR_SMEM_REPL, 1, 0, bad_flags)
+        assert _call(rk, 10, A, A, 4, cfg=cfg) == _native.AES_ERANGE
+    cfg = _native.aes_launch_config(_native.AES_VAR_GLOBAL, 2, 0, 0)
+    assert _call(rk, 10, A, A, 4, cfg=cfg) == _native.AES_EVARIANT
     # a tampered schedule (keybits inconsistent with nr) is rejected
     bad = aes.expand_key(bytes(16))
     bad.c.keybits = 256

@@ -13,15 +13,16 @@ from paper_1902_05234_b200 import _native
 import paper_1902_05234_b200 as aes
 
 PTRS = st.sampled_from([0, 16, 0x10000, 0x10008, 0x10010, 2**47 - 16, 2**63 - 16])
-CODES = set(range(10))
+CODES = set(range(11))
 
 
 @settings(max_examples=400, deadline=None, derandomize=True)
 @given(nr=st.integers(-2, 20), inp=PTRS, out=PTRS, n=st.sampled_from([0, 1, 2, 31, 2**20, 2**40, 2**59, 2**60, 2**64 - 1]),
-       dec=st.integers(0, 1), variant=st.integers(-1, 8), spt=st.integers(-1, 5), grid=st.integers(-2, 3))
-def test_launch_validation_total(nr, inp, out, n, dec, variant, spt, grid):
+       dec=st.integers(0, 1), variant=st.integers(-1, 8), spt=st.integers(-1, 5), grid=st.integers(-2, 3),
+       flags=st.integers(-1, 5))
+def test_launch_validation_total(nr, inp, out, n, dec, variant, spt, grid, flags):
     rk = aes.expand_key(bytes(16))
-    cfg = _native.aes_launch_config(variant, spt, grid, 0)
+    cfg = _native.aes_launch_config(variant, spt, grid, flags)
     code = _native.lib.aes_ecb_launch(ctypes.byref(rk.c), nr, dec, inp, out, n, None, ctypes.byref(cfg))
     assert code in CODES
     if nr != 10:

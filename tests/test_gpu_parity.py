@@ -18,8 +18,9 @@ import oracle
 import synth
 from conftest import golden
 
-VARIANTS = [(1, 1), (1, 2), (1, 4), (2, 1), (3, 1), (4, 1), (5, 1)]   # (variant, states_per_thread)
-SIZES = [1, 2, 31, 32, 33, 1023, 1024, 1025, 4096 + 17, 148 * 1024 + 7, 65536]
+VARIANTS = [(1, 1), (1, 2), (1, 4), (2, 1), (3, 1), (4, 1), (5, 1), (6, 1)]   # (variant, states_per_thread)
+# one warp .. several CTAs, ragged tails, 1 MiB, and whole grid-stride trips + a per-CTA tail split
+SIZES = [1, 2, 31, 32, 33, 1023, 1024, 1025, 4096 + 17, 148 * 1024 + 7, 65536, 2 * 148 * 1024 + 30011]
 
 
 @pytest.fixture(scope="module")
@@ -588,3 +589,96 @@ def test_pipeline_unaligned_host_buffers(aes):
     p.run(rk, src, dst)
     assert np.array_equal(dst.numpy(), oracle.encrypt(key, host, nthreads=4))
     p.close()
+
+
+def test_launch_flags_trusted_pointers_and_no_pdl(aes):
+    """aes_launch_config.flags: TRUSTED_PTRS (no per-call pointer queries) and
+    NO_PDL give the same bytes as the default (checked pointers + PDL)."""
+    from paper_1902_05234_b200 import _native
+    key = synth.key(192)
+    rk = aes.expand_key(key)
+    n = 70001
+    x = _dev_rand(n, first=3)
+    want = oracle.encrypt(key, synth.blocks(3, n), nthreads=8)
+    for fl in (0, aes.AES_LAUNCH_TRUSTED_PTRS, aes.AES_LAUNCH_NO_PDL, aes.AES_LAUNCH_TRUSTED_PTRS | aes.AES_LAUNCH_NO_PDL):
+        ct = aes.ecb_encrypt(rk, x, flags=fl)
+        assert np.array_equal(ct.cpu().numpy(), want), fl
+        assert torch.equal(aes.ecb_decrypt(rk, ct, flags=fl), x), fl
+    cfg = _native.aes_launch_config(0, 0, 0, 4)
+    code = _native.lib.aes_ecb_launch(rk.c_ref, 12, 0, x.data_ptr(), x.data_ptr(), n, None, ctypes.byref(cfg))
+    assert code == _native.AES_ERANGE
+
+
+def test_back_to_back_pdl_chain_in_place(aes):
+    """A chain of dependent in-place launches (each kernel reads what the
+    previous one wrote) with PDL overlap: 2k+1 alternating encrypt/decrypt
+    launches == one encrypt, for sizes from one warp to several trips, eagerly
+    and inside a CUDA graph."""
+    key = synth.key(128)
+    rk = aes.expand_key(key)
+    s = torch.cuda.Stream()
+    for n in (32, 4099, 65536, 148 * 1024 * 3 + 77):
+        x = _dev_rand(n, first=n)
+        want = oracle.encrypt(key, synth.blocks(n, n), nthreads=8)
+        y = x.clone()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s):
+            for k in range(41):
+                aes.ecb(rk, y, decrypt=bool(k & 1), out=y)
+        s.synchronize()
+        assert np.array_equal(y.cpu().numpy(), want), n
+        y.copy_(x)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for k in range(21):
+                    aes.ecb(rk, y, decrypt=bool(k & 1), out=y)
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy(), want), ("graph", n)
+
+
+def test_prepared_call_fast_path(aes):
+    """EcbCall: validated once, then each call is one C-ABI launch with trusted
+    pointers on the current stream; same bytes as the checked path."""
+    key = synth.key(256)
+    rk = aes.expand_key(key)
+    n = 65536 + 3
+    x = _dev_rand(n, first=11)
+    out = torch.empty_like(x)
+    enc = aes.prepare_ecb(rk, x, out)
+    dec = aes.prepare_ecb(rk, out, out, decrypt=True)     # in place
+    assert enc() is out
+    assert np.array_equal(out.cpu().numpy(), oracle.encrypt(key, synth.blocks(11, n), nthreads=8))
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    dec(stream=s)
+    s.synchronize()
+    assert torch.equal(out, x)
+    with pytest.raises(aes.AesError):                     # partial overlap
+        aes.prepare_ecb(rk, x[16:], x[:-16])
+    z = torch.zeros(64 + 8, dtype=torch.uint8, device="cuda")
+    with pytest.raises(aes.AesError):                     # misaligned view
+        aes.prepare_ecb(rk, z[8:], torch.empty(64, dtype=torch.uint8, device="cuda"))
+    with pytest.raises(TypeError):
+        aes.prepare_ecb(rk, x.cpu())
+
+
+def test_small_message_work_split_every_cta_busy(aes):
+    """Messages below one grid-stride trip are split into per-CTA chunks:
+    parity at sizes around the chunk rounding (multiples of 32 per CTA) and
+    with explicit grids, for every key size and direction."""
+    for kb in (128, 256):
+        key = synth.key(kb)
+        rk = aes.expand_key(key)
+        for n in (33, 148 * 32 - 1, 148 * 32 + 1, 74401, 148 * 1024 - 1):
+            x = _dev_rand(n, first=7 * n)
+            host = synth.blocks(7 * n, n)
+            want = oracle.encrypt(key, host, nthreads=8)
+            wantd = oracle.decrypt(key, host, nthreads=8)
+            for grid in (0, 5, 148):
+                assert np.array_equal(aes.ecb_encrypt(rk, x, grid=grid, variant=1).cpu().numpy(), want), (kb, n, grid)
+                assert np.array_equal(aes.ecb_decrypt(rk, x, grid=grid, variant=1).cpu().numpy(), wantd), (kb, n, grid)
+            cbc = aes.cbc_decrypt(rk, bytes(16), x)
+            assert np.array_equal(cbc.cpu().numpy(), oracle.cbc(key, bytes(16), host, decrypt=True)), (kb, n)
