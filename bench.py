@@ -7,8 +7,11 @@ A STEP = one pass of the whole hot path over one
 batch: aes_expand_key (host) -> aes_ecb_encrypt(1 GiB) -> aes_ecb_decrypt of
 that ciphertext (1 GiB).  Payload per step and rank = 2 GiB.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
-For N > 1 launch under torchrun (one rank per GPU; NCCL only for barrier and
-the MAX/SUM of scalars -- no data-path collective).
+For N > 1: one rank per GPU (NCCL only for barrier and the MAX/SUM of
+scalars -- no data-path collective).  Under torchrun
+(--nproc-per-node N) the ranks come from the env; without torchrun the
+script re-launches itself under torch.distributed.run with N processes.
+Either way it refuses to run unless WORLD_SIZE == --gpus.
 Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
@@ -440,8 +443,17 @@ def run_ours(a):
     e2e = None if a.no_e2e else _e2e(aes, pdist, key, rk, x, ct, pt, nbytes, K, dev)
     roof, roof_lds, peak = _rooflines(n, enc_ms, dec_ms, lds_peak, nsm, clocks)
 
+    # per-rank spread: kernel and step times, devices used
+    ranks = {"world": world, "backend": pdist.backend_name(),
+             "step_ms_min": pdist.min_over_ranks(ms_local, dev), "step_ms_max": ms,
+             "kernel_ms_min": pdist.min_over_ranks(max(enc_ms, dec_ms), dev),
+             "kernel_ms_max": pdist.max_over_ranks(max(enc_ms, dec_ms), dev),
+             "devices": pdist.gather_objects(f"{torch.cuda.get_device_name(dev)}#{dev.index}"
+                                             f"@{torch.cuda.get_device_properties(dev).uuid}"),
+             "skew_ms": wall_ms - ms}
+
     cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu:
+    if rank == 0 and not a.no_cpu:
         cores = host_cores()
         g, sample, _ = time_oracle(a.cpu_seconds, cores)
         g1, sample1, _ = time_oracle(min(3.0, a.cpu_seconds), 1)
@@ -471,7 +483,7 @@ def run_ours(a):
                               "AES-128 ECB cannot exceed ~28% of HBM on B200 (DESIGN.md 6, 11)"),
             "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clocks, "gpu_launches": 2 * K, "gpu": torch.cuda.get_device_name(dev),
-            "wall_window_ms_rank0": wall_ms,
+            "wall_window_ms_rank0": wall_ms, "ranks": ranks,
             "context": {"ctr_aes128_Gbps": ctr_gbps,
                         "note": "NEXT-1 CTR (counter-mode caching) on the same 1 GiB buffer; not part of `value`"},
         }
@@ -485,6 +497,13 @@ def main():
     a = parse()
     if a.impl == "reference":
         return run_reference(a)
+    import __graft_entry__
+    __graft_entry__.build()               # once, before any rank exists (no-op when up to date)
+    from paper_1902_05234_b200.dist import require_world, respawn_under_torchrun
+    rc = respawn_under_torchrun(a.gpus, [os.path.abspath(__file__), *sys.argv[1:]])
+    if rc is not None:
+        return rc
+    require_world(a.gpus)
     return run_ours(a)
 
 

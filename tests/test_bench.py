@@ -54,12 +54,34 @@ def test_bench_our_arm_n1():
 
 @pytest.mark.gpu
 def test_bench_n2_code_path_with_gloo_on_one_gpu():
+    """Driver-style launch: torchrun --nproc-per-node 2 ... bench.py --gpus 2."""
     env = dict(os.environ, AES_BENCH_BACKEND="gloo")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
-                        "--steps", "3", "--warmup", "3", "--bytes-per-gpu", str(32 << 20)],
+                        "--steps", "3", "--warmup", "3", "--bytes-per-gpu", str(32 << 20), "--cpu-seconds", "1"],
                        cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     d = _last_json(r.stdout)
     assert d["n_gpus"] == 2 and d["config"]["global_bytes"] == 2 * (32 << 20)
-    assert d["cpu_baseline"] is None and d["gpu_launches"] == 6
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["gpu_launches"] == 6
+    assert d["ranks"]["world"] == 2 and len(d["ranks"]["devices"]) == 2
+
+
+@pytest.mark.gpu
+def test_bench_gpus_2_without_torchrun_spawns_its_ranks():
+    """`python bench.py --gpus 2` with no launcher re-launches itself with two
+    ranks (here both on the one GPU of the test box, gloo): n_gpus 2, twice
+    the bytes, cpu_baseline from rank 0."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["AES_BENCH_BACKEND"] = "gloo"
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3",
+                        "--bytes-per-gpu", str(32 << 20), "--cpu-seconds", "1"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["global_bytes"] == 2 * (32 << 20)
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["ranks"]["world"] == 2 and d["ranks"]["backend"] == "gloo"
+    assert d["ranks"]["kernel_ms_min"] <= d["ranks"]["kernel_ms_max"]

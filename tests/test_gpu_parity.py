@@ -206,6 +206,41 @@ def test_config3_aes256_4gib_decrypt_sampled(aes):
     del x, ct
 
 
+def test_config3_aes256_4gib_decrypt_full_parity(aes):
+    """BASELINE config 3, FULL parity (Table 5,
+    PAPER.md:525-553): the GPU decrypts the whole 4 GiB AES-256 buffer (the
+    splitmix64 stream read as ciphertext; byte offsets >= 2^32) in the bench's
+    launch configuration, and every one of its 2^28 blocks is compared with
+    the oracle's InvCipher of the host twin of the same stream, chunk by chunk
+    on all host cores.  Then the GPU round trip E(D(x)) == x."""
+    import os
+    import time
+    free, _ = torch.cuda.mem_get_info()
+    if free < 10 * (1 << 30):
+        pytest.skip("needs ~10 GiB free")
+    n = (4 << 30) // 16
+    key = synth.key(256)
+    rk = aes.expand_key(key)
+    x = _dev_rand(n)
+    pt = aes.ecb_decrypt(rk, x)
+    torch.cuda.synchronize()
+    cores = len(os.sched_getaffinity(0))
+    chunk = 1 << 22                                    # 64 MiB of host memory per side
+    t0 = time.perf_counter()
+    for first in range(0, n, chunk):
+        nb = min(chunk, n - first)
+        want = oracle.decrypt(key, synth.blocks(first, nb), nthreads=cores)
+        got = pt[16 * first:16 * (first + nb)].cpu().numpy()
+        if not np.array_equal(got, want):
+            bad = np.nonzero((got.reshape(-1, 16) != want.reshape(-1, 16)).any(axis=1))[0]
+            pytest.fail(f"AES-256 decrypt mismatch: first bad block {first + int(bad[0])} "
+                        f"({len(bad)} bad blocks in chunk at {first})")
+    print(f"config 3 full parity: {n} blocks on {cores} cores in {time.perf_counter() - t0:.1f} s")
+    back = aes.ecb_encrypt(rk, pt, out=pt)
+    assert torch.equal(back, x)
+    del x, pt
+
+
 def test_lds_gather_microbenchmark_runs(aes):
     sink = torch.zeros(148 * 1024, dtype=torch.int32, device="cuda")
     aes.lds_gather(sink, 148, 4)

@@ -3,7 +3,8 @@
 sharded across N GPUs -- strong scaling (total work fixed).
 
     python tools/scale.py                                   # N = 1 (64 GiB on one GPU, in place)
-    torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/scale.py
+    python tools/scale.py --gpus N                          # spawns N ranks itself
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/scale.py --gpus N
 
 Rank r owns blocks [r*n/N, (r+1)*n/N) of the global splitmix64 stream
 (dist.shard_range), fills them on its own GPU, checks sampled blocks against
@@ -28,12 +29,22 @@ from paper_1902_05234_b200 import dist as pdist
 from synth import golden
 
 
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    return float(json.load(open(p))["hbm_gbs"]) if os.path.exists(p) else 6650.0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--global-bytes", type=int, default=64 << 30)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", 1)))
     a = ap.parse_args()
+    rc = pdist.respawn_under_torchrun(a.gpus, [os.path.abspath(__file__), *sys.argv[1:]])
+    if rc is not None:
+        return rc
+    pdist.require_world(a.gpus)
     rank, world, local = pdist.init(os.environ.get("AES_BENCH_BACKEND") or None)
     dev = torch.device("cuda", local % torch.cuda.device_count())
     torch.cuda.set_device(dev)
@@ -81,7 +92,10 @@ def main():
         e1.record(s)
     s.synchronize()
     pdist.barrier(dev)
-    ms = pdist.max_over_ranks(e0.elapsed_time(e1), dev)
+    ms_local = e0.elapsed_time(e1)
+    ms = pdist.max_over_ranks(ms_local, dev)
+    ms_min = pdist.min_over_ranks(ms_local, dev)
+    devices = pdist.gather_objects(f"{torch.cuda.get_device_name(dev)}#{dev.index}")
     total = pdist.sum_over_ranks(16.0 * m * a.steps, dev)
     if rank == 0:
         gbps = 8 * total / (ms * 1e-3) / 1e9
@@ -89,9 +103,13 @@ def main():
                           "value": gbps, "unit": "Gbps", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
                           "ms_per_step": ms / a.steps, "scaling": "strong", "global_bytes": a.global_bytes,
                           "bytes_per_gpu": 16 * m, "GBps": gbps / 8,
-                          "hbm_frac": 32 * total / 16 / (ms * 1e-3) / 1e9 / 6550.7 / world,
+                          "hbm_frac": 32 * total / 16 / (ms * 1e-3) / 1e9 / hbm_peak() / world,
                           "parity": "golden (oracle-written) samples incl. shard edges and block 2^32-1; in-place round trip on the samples",
+                          "ranks": {"world": world, "backend": pdist.backend_name(), "ms_min": ms_min,
+                                    "ms_max": ms, "devices": devices},
                           "gpu": torch.cuda.get_device_name(dev)}), flush=True)
+    pdist.barrier(dev)
+    pdist.finalize()
     return 0
 
 

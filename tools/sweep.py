@@ -87,7 +87,33 @@ def time_op(fn, s, reps, flush=None):
     return min(ts), statistics.median(ts)
 
 
-def time_b2b(fn, s, reps):
+def time_graph_b2b(fn, s, reps):
+    """Per-launch DEVICE time of `reps` back-to-back launches captured in a CUDA
+    graph and replayed between two events (no host enqueue cost inside)."""
+    g = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                fn()
+    g.replay()
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record(s)
+            g.replay()
+            e1.record(s)
+        s.synchronize()
+        best = min(best, e0.elapsed_time(e1) * 1e-3 / reps)
+    del g
+    return best
+
+
+def time_eager_b2b(fn, s, reps):
+    """Mean time per launch of `reps` eager launches issued back to back (the
+    host enqueue cost bounds it when a launch is shorter than its call)."""
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(s):
         fn()
@@ -97,6 +123,37 @@ def time_b2b(fn, s, reps):
         e1.record(s)
     s.synchronize()
     return e0.elapsed_time(e1) * 1e-3 / reps
+
+
+def time_device_single(fn, s, reps, flush=None):
+    """One launch between two events, queued behind a GPU spin so the host
+    enqueue cost is outside the interval (isolated-launch device time)."""
+    ts = []
+    for _ in range(reps):
+        with torch.cuda.stream(s):
+            if flush is not None:
+                flush.zero_()
+            torch.cuda._sleep(40000)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            fn()
+            e1.record(s)
+        s.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e-3)
+    return min(ts), statistics.median(ts)
+
+
+def time_host_call(fn, reps=200):
+    """Host cost of one call (Python wrapper -> C ABI -> cudaLaunchKernelExC),
+    mean over back-to-back calls."""
+    import time
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        fn()
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    return (t1 - t0) / reps
 
 
 def record(**kw):
@@ -129,24 +186,32 @@ def sizes(a, s, hbm, ldsp):
                     f()
                 torch.cuda.synchronize()   # warm-ups ran on the default stream; s is non-blocking
                 tmin, tmed = time_op(f, s, reps, None if warm else flush)
-                tb2b = time_b2b(f, s, 20 if nbytes < (256 << 20) else 3)
-                g = 8 * nbytes / tmin / 1e9
-                fits.setdefault((kb, dec), []).append((n, tmin))
-                record(what="size", bytes=nbytes, keybits=kb, dir="dec" if dec else "enc", t_min_s=tmin,
-                       t_med_s=tmed, Gbps=g, GBps=g / 8, hbm_frac=32 * n / tmin / 1e9 / hbm,
-                       lds_frac=16 * NR[kb] * n / tmin / ldsp, l2="flushed" if not warm else "input>2xL2",
-                       t_b2b_s=tb2b, Gbps_b2b=8 * nbytes / tb2b / 1e9,
-                       note="t_min: one call incl. host launch path (L2 flushed if small); "
-                            "t_b2b: mean of back-to-back launches (device time, L2 warm if small)")
+                dmin, dmed = time_device_single(f, s, reps, None if warm else flush)
+                tb2b = time_graph_b2b(f, s, 20) if nbytes < (256 << 20) else dmin
+                thost = time_host_call(f, 200 if nbytes < (16 << 20) else 5)
+                g = 8 * nbytes / dmin / 1e9
+                fits.setdefault((kb, dec), []).append((n, dmin, tb2b))
+                record(what="size", bytes=nbytes, keybits=kb, dir="dec" if dec else "enc",
+                       t_call_min_s=tmin, t_call_med_s=tmed, t_device_min_s=dmin, t_device_med_s=dmed,
+                       t_graph_b2b_s=tb2b, t_host_call_s=thost, Gbps=g, GBps=g / 8,
+                       Gbps_graph_b2b=8 * nbytes / tb2b / 1e9,
+                       hbm_frac=32 * n / dmin / 1e9 / hbm, lds_frac=16 * NR[kb] * n / dmin / ldsp,
+                       l2="flushed" if not warm else "input>2xL2",
+                       note="t_call: events around one call incl. host enqueue; t_device: one launch queued "
+                            "behind a GPU spin (device time of an isolated launch, L2 flushed if small); "
+                            "t_graph_b2b: per-launch device time of 20 back-to-back launches in a CUDA graph "
+                            "(PDL overlap, L2 warm if small; = t_device for >= 256 MiB); t_host_call: host "
+                            "cost of one Python-wrapper call")
         del x, out
         torch.cuda.empty_cache()
     for (kb, dec), pts in fits.items():
         nn = np.array([p[0] for p in pts], float)
-        tt = np.array([p[1] for p in pts], float)
         A = np.stack([np.ones_like(nn), nn], 1)
-        (t0, inv), *_ = np.linalg.lstsq(A, tt, rcond=None)
-        record(what="fit", keybits=kb, dir="dec" if dec else "enc", t0_us=t0 * 1e6,
-               R_inf_GBps=16 / inv / 1e9 if inv > 0 else None)
+        for col, which in ((1, "device_single"), (2, "graph_b2b")):
+            tt = np.array([p[col] for p in pts], float)
+            (t0, inv), *_ = np.linalg.lstsq(A, tt, rcond=None)
+            record(what="fit", keybits=kb, dir="dec" if dec else "enc", timing=which, t0_us=t0 * 1e6,
+                   R_inf_GBps=16 / inv / 1e9 if inv > 0 else None)
 
 
 def variants(a, s, hbm, ldsp):
@@ -156,10 +221,11 @@ def variants(a, s, hbm, ldsp):
     n = nbytes // 16
     key = synth.key(128)
     rk = aes.expand_key(key)
-    names = {1: "smem_repl", 2: "smem_plain", 3: "const (paper)", 4: "smem_repl + TMA staging", 5: "one table + rotations"}
+    names = {1: "smem_repl", 2: "smem_plain", 3: "const (paper)", 4: "smem_repl + TMA staging", 5: "one table + rotations",
+             6: "global __ldg (L1)"}
     for kind in ("random", "zeros", "repeat", "ascii"):
         synth.fill_device(x, kind=kind)
-        for v, spt in ((1, 1), (1, 2), (1, 4), (4, 1), (5, 1), (2, 1), (3, 1)):
+        for v, spt in ((1, 1), (1, 2), (1, 4), (4, 1), (5, 1), (2, 1), (6, 1), (3, 1)):
             if kind != "random" and (v == 1 and spt != 1 or v in (4, 5)):
                 continue
             for dec in (False, True):
@@ -170,7 +236,7 @@ def variants(a, s, hbm, ldsp):
                     parity(128, out, "ecb_dec" if dec else "ecb_enc")
                 else:
                     assert torch.equal(out, aes.ecb(rk, x, dec)), ("variant mismatch", v, spt, kind)
-                reps = 10 if v != 3 else 3
+                reps = 10 if v not in (3, 6) else 3
                 tmin, tmed = time_op(f, s, reps)
                 g = 8 * nbytes / tmin / 1e9
                 record(what="variant", variant=names[v], spt=spt, data=kind, dir="dec" if dec else "enc",
@@ -257,9 +323,17 @@ def modes(a, s, hbm, ldsp):
             torch.cuda.synchronize()   # warm-ups ran on the default stream; s is non-blocking
             tmin, tmed = time_op(f, s, 10)
             g = 8 * nbytes / tmin / 1e9
+            # the method's own work: CTR with counter-mode caching does 16(Nr-2)+5 lookups per
+            # block plus 27 per warp per 16 trips for its group tables (27/512 per block);
+            # CBC decryption moves 32 DRAM bytes per block (the neighbour block re-read
+            # hits L1/L2) while requesting 48
+            looks = 16 * (NR[kb] - 2) + 5 + 27 / 512 if mode == "ctr" else 16 * NR[kb]
             record(what="mode", mode=mode, keybits=kb, bytes=nbytes, t_min_s=tmin, t_med_s=tmed, Gbps=g,
-                   hbm_frac=(48 if mode == "cbc_dec" else 32) * n / tmin / 1e9 / hbm,
-                   lds_frac=16 * NR[kb] * n / tmin / ldsp)
+                   hbm_frac=32 * n / tmin / 1e9 / hbm,
+                   requested_bytes_per_block=48 if mode == "cbc_dec" else 32,
+                   lookups_per_block=looks, lds_frac=looks * n / tmin / ldsp,
+                   note="hbm_frac counts 32 DRAM bytes per block (16 read + 16 written); lds_frac counts the "
+                        "lookups this kernel performs")
 
 
 def batch(a, s, hbm, ldsp):
@@ -293,7 +367,7 @@ def batch(a, s, hbm, ldsp):
             fbatch()
         torch.cuda.synchronize()
         tb, _ = time_op(fbatch, s, 10)
-        tbd = time_b2b(fbatch, s, 10)          # back to back: device-bound rate
+        tbd = time_eager_b2b(fbatch, s, 10)     # back to back, eager (aes_ecb_batch is not graph-capturable)
         # M separate calls, back to back (host launch path included, as a user would see it)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
