@@ -318,11 +318,14 @@ def ecb_batch(rks, xs, outs=None, key_index=None, decrypt: bool = False, stream=
         outs = [torch.empty_like(x) for x in xs]
     if len(outs) != n:
         raise ValueError("one output per message")
+    dev0 = xs[0].device if n else None
     for x, o in zip(xs, outs):
         _check_tensor(x, "x")
         _check_tensor(o, "out")
         if o.numel() != x.numel():
             raise ValueError("out must match x")
+        if x.device != dev0 or o.device != dev0:
+            raise ValueError("all messages and outputs must be on one CUDA device")
     live = [i for i in range(n) if xs[i].numel()]
     if not live:
         return outs

@@ -31,6 +31,12 @@ KEYS = [
     ("smsp__sass_inst_executed_op_shared_ld.sum", "LDS instructions"),
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "LDS wavefronts"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "LDS bank conflicts"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "global-load requests (L1 tag stage)"),
+    ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "global-load sectors"),
+    ("l1tex__t_sector_pipe_lsu_mem_global_op_ld_hit_rate.pct", "global-load L1 hit rate"),
+    ("l1tex__t_output_wavefronts_pipe_lsu_mem_global_op_ld.sum", "global-load L1 output wavefronts"),
+    ("idc__requests.sum", "constant-cache (IDC) requests"),
+    ("idc__request_hit_rate.pct", "constant-cache hit rate"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
     ("launch__registers_per_thread", "registers/thread"),
     ("launch__shared_mem_per_block_dynamic", "dyn smem/CTA"),
