@@ -168,7 +168,15 @@ aes_status aes_ecb_batch(const aes_round_keys *keys, int nkeys, int decrypt, con
  *                       as funnel-shift rotations (Eqs 23-25 are byte rotations
  *                       of Eq 22): 64 KiB of shared memory instead of 128/192.
  *  AES_VAR_GLOBAL     : tables left in global memory, read through the
- *                       read-only L1 path (__ldg); no shared memory. */
+ *                       read-only L1 path (__ldg); no shared memory.
+ *  AES_VAR_HYBRID     : SMEM_REPL T-table warps plus, in the same CTA, warps
+ *                       that run a bitsliced (lookup-free, Boolean-circuit
+ *                       S-box) cipher on the integer pipe the table lookups
+ *                       leave idle; both take 32-block units from a per-CTA
+ *                       queue.  states_per_thread must be 1.
+ *  AES_VAR_BITSLICE   : every warp bitsliced (8 blocks per thread), no tables;
+ *                       the ALU-only point of the ablation.  states_per_thread
+ *                       must be 1. */
 typedef enum {
     AES_VAR_DEFAULT = 0,
     AES_VAR_SMEM_REPL = 1,
@@ -176,7 +184,9 @@ typedef enum {
     AES_VAR_CONST = 3,
     AES_VAR_SMEM_REPL_TMA = 4,
     AES_VAR_SMEM_ROT = 5,
-    AES_VAR_GLOBAL = 6
+    AES_VAR_GLOBAL = 6,
+    AES_VAR_HYBRID = 7,
+    AES_VAR_BITSLICE = 8
 } aes_variant;
 
 /* aes_launch_config.flags (bitwise OR):

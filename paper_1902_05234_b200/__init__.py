@@ -15,14 +15,15 @@ from __future__ import annotations
 import ctypes
 
 from . import _native
-from ._native import (AES_LAUNCH_NO_PDL, AES_LAUNCH_TRUSTED_PTRS, AES_VAR_CONST, AES_VAR_DEFAULT, AES_VAR_GLOBAL,
-                      AES_VAR_SMEM_PLAIN, AES_VAR_SMEM_REPL, AES_VAR_SMEM_REPL_TMA, AES_VAR_SMEM_ROT, aes_launch_config,
+from ._native import (AES_LAUNCH_NO_PDL, AES_LAUNCH_TRUSTED_PTRS, AES_VAR_BITSLICE, AES_VAR_CONST, AES_VAR_DEFAULT,
+                      AES_VAR_GLOBAL, AES_VAR_HYBRID, AES_VAR_SMEM_PLAIN, AES_VAR_SMEM_REPL, AES_VAR_SMEM_REPL_TMA, AES_VAR_SMEM_ROT, aes_launch_config,
                       aes_round_keys, status_string)
 
 __all__ = ["RoundKeys", "expand_key", "ecb_encrypt", "ecb_decrypt", "ecb", "ecb_batch", "ecb_batch_offsets", "KeySet", "ctr_xcrypt", "cbc_decrypt",
            "ecb_trace", "Pipeline",
            "lds_gather", "AesError", "AES_VAR_DEFAULT", "AES_VAR_SMEM_REPL", "AES_VAR_SMEM_PLAIN",
-           "AES_VAR_CONST", "AES_VAR_SMEM_REPL_TMA", "AES_VAR_SMEM_ROT", "AES_VAR_GLOBAL", "AES_LAUNCH_TRUSTED_PTRS",
+           "AES_VAR_CONST", "AES_VAR_SMEM_REPL_TMA", "AES_VAR_SMEM_ROT", "AES_VAR_GLOBAL", "AES_VAR_HYBRID", "AES_VAR_BITSLICE",
+           "AES_LAUNCH_TRUSTED_PTRS",
            "AES_LAUNCH_NO_PDL", "abi_version", "prepare_ecb", "EcbCall"]
 
 

@@ -16,7 +16,7 @@ AES_OK, AES_EKEYBITS, AES_ENR, AES_ENULL, AES_EALIGN, AES_EOVERLAP, AES_ERANGE, 
     AES_ENOTDEVICE, AES_ECUDA, AES_EVARIANT, AES_ECAPTURE = range(11)
 
 AES_VAR_DEFAULT, AES_VAR_SMEM_REPL, AES_VAR_SMEM_PLAIN, AES_VAR_CONST, AES_VAR_SMEM_REPL_TMA, AES_VAR_SMEM_ROT, \
-    AES_VAR_GLOBAL = range(7)
+    AES_VAR_GLOBAL, AES_VAR_HYBRID, AES_VAR_BITSLICE = range(9)
 AES_LAUNCH_TRUSTED_PTRS, AES_LAUNCH_NO_PDL = 1, 2
 
 # every symbol include/aes_b200.h declares

@@ -79,7 +79,7 @@ constexpr size_t kSmemReplDec = 2 * kRegion + 255 * 256 + 128;
 constexpr size_t kSmemPlain = (4 * 256 + 256) * 4;
 constexpr size_t kSmemRot = 255 * 256 + 256;   // one replicated table (+ Si4 for decryption) in a 64 KiB region
 
-enum { V_REPL = 1, V_PLAIN = 2, V_CONST = 3, V_REPL_TMA = 4, V_ROT = 5, V_GLOBAL = 6 };
+enum { V_REPL = 1, V_PLAIN = 2, V_CONST = 3, V_REPL_TMA = 4, V_ROT = 5, V_GLOBAL = 6, V_HYBRID = 7, V_BITSLICE = 8 };
 
 // ---------------------------------------------------------------------------
 // Programmatic dependent launch (PDL).  Every kernel lets the next kernel of

@@ -36,6 +36,7 @@
 #include <cstring>
 
 #include "aes_b200.h"
+#include "aes_bitslice.cuh"
 #include "aes_device.cuh"
 #include "aes_host.h"
 
@@ -450,7 +451,10 @@ aes_status launch(const aes_round_keys* rk, int nr, int decrypt, const void* in,
     if (spt == 0) spt = 1;                              // S = 1, 2, 4 measure within 1 %
     if (grid_req < 0 || (flags & ~(AES_LAUNCH_TRUSTED_PTRS | AES_LAUNCH_NO_PDL))) return AES_ERANGE;
     if (flags & AES_LAUNCH_TRUSTED_PTRS) check_ptrs = false;
-    KernelInfo ki = mode == M_ECB ? pick(nr, decrypt != 0, variant, spt) : pick_mode(nr, mode);
+    bool bsk = mode == M_ECB && (variant == V_HYBRID || variant == V_BITSLICE);
+    KernelInfo ki = mode != M_ECB ? pick_mode(nr, mode)
+                    : bsk         ? (spt == 1 ? pick_hybrid(nr, decrypt != 0, variant) : KernelInfo{nullptr, 0})
+                                  : pick(nr, decrypt != 0, variant, spt);
     if (mode != M_ECB) spt = 1;
     if (!ki.fn) return AES_EVARIANT;
     if (nblocks == 0) return AES_OK;
@@ -473,12 +477,24 @@ aes_status launch(const aes_round_keys* rk, int nr, int decrypt, const void* in,
     uint64_t want = (nblocks + per_cta - 1) / per_cta;
     uint64_t cap = grid_req ? (uint64_t)grid_req : (uint64_t)nsm * occ;
     unsigned grid = (unsigned)(want < cap ? want : cap);
+    if (bsk && variant == V_HYBRID && (nblocks / 32) / grid >= (1ull << 31) - 64) {
+        // beyond the hybrid kernel's 32-bit per-CTA unit counter (2^36 blocks per
+        // CTA = 1 TiB): the T-table kernel computes the identical result
+        bsk = false;
+        ki = pick(nr, decrypt != 0, V_REPL, 1);
+        if ((st = resident_ctas(dev, ki, &occ, &nsm))) return st;
+    }
     RK k;
     std::memcpy(k.w, decrypt ? rk->dk : rk->ek, sizeof k.w);
     const uint4* pin = static_cast<const uint4*>(in);
     uint4* pout = static_cast<uint4*>(out);
     ModeP m = mp ? *mp : ModeP{};
     void* args[] = {(void*)&pin, (void*)&pout, (void*)&nblocks, (void*)&k, (void*)&m};
+    if (bsk) {   // hybrid / bitsliced kernels take the bitsliced round keys instead of ModeP
+        static thread_local BSK bs;
+        bitslice_keys(rk, decrypt, &bs);
+        args[4] = (void*)&bs;
+    }
     return launch_kernel(ki, grid, args, stream, !(flags & AES_LAUNCH_NO_PDL));
 }
 

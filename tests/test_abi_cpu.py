@@ -115,8 +115,11 @@ def test_validation_errors_before_any_cuda_call():
     assert _call(rk, 10, A, A + 16, 4) == _native.AES_EOVERLAP
     assert _call(rk, 10, A + 16, A, 4) == _native.AES_EOVERLAP
     assert _call(rk, 10, A, A, 1 << 62) == _native.AES_ERANGE
-    cfg = _native.aes_launch_config(7, 0, 0, 0)
+    cfg = _native.aes_launch_config(9, 0, 0, 0)                 # unknown variant
     assert _call(rk, 10, A, A, 4, cfg=cfg) == _native.AES_EVARIANT
+    for v in (_native.AES_VAR_HYBRID, _native.AES_VAR_BITSLICE):   # one state per thread only
+        cfg = _native.aes_launch_config(v, 2, 0, 0)
+        assert _call(rk, 10, A, A, 4, cfg=cfg) == _native.AES_EVARIANT
     cfg = _native.aes_launch_config(_native.AES_VAR_SMEM_REPL, 3, 0, 0)
     assert _call(rk, 10, A, A, 4, cfg=cfg) == _native.AES_EVARIANT
     cfg = _native.aes_launch_config(_native.AES_VAR_SMEM_REPL_TMA, 2, 0, 0)

@@ -18,7 +18,7 @@ import oracle
 import synth
 from conftest import golden
 
-VARIANTS = [(1, 1), (1, 2), (1, 4), (2, 1), (3, 1), (4, 1), (5, 1), (6, 1)]   # (variant, states_per_thread)
+VARIANTS = [(1, 1), (1, 2), (1, 4), (2, 1), (3, 1), (4, 1), (5, 1), (6, 1), (7, 1), (8, 1)]   # (variant, states_per_thread)
 # one warp .. several CTAs, ragged tails, 1 MiB, and whole grid-stride trips + a per-CTA tail split
 SIZES = [1, 2, 31, 32, 33, 1023, 1024, 1025, 4096 + 17, 148 * 1024 + 7, 65536, 2 * 148 * 1024 + 30011]
 
@@ -95,6 +95,33 @@ def test_small_grids_many_trips_and_in_place(aes):
     assert np.array_equal(y.cpu().numpy(), want)
     aes.ecb_decrypt(rk, y, out=y)
     assert torch.equal(y, x)
+
+
+@pytest.mark.parametrize("keybits", [128, 192, 256])
+def test_hybrid_both_paths_against_oracle(aes, keybits):
+    """AES_VAR_HYBRID with few CTAs: each CTA then needs > kTailUnits units, so
+    its bitsliced warps take part (they stop claiming kTailUnits units before
+    the end) next to the T-table warps; ragged tail, in place, both directions."""
+    key = synth.key(keybits)
+    rk = aes.expand_key(key)
+    for n, grid in ((65536 + 1234, 1), (3 * 32 * 1024 + 77, 3), (148 * 32 * 400 + 5, 148)):
+        x = _dev_rand(n, first=7 * n)
+        src = synth.blocks(7 * n, n)
+        want_ct = oracle.encrypt(key, src, nthreads=16)
+        want_pt = oracle.decrypt(key, src, nthreads=16)
+        ct = aes.ecb_encrypt(rk, x, grid=grid, variant=aes.AES_VAR_HYBRID)
+        assert np.array_equal(ct.cpu().numpy(), want_ct), (keybits, n, grid)
+        pt = aes.ecb_decrypt(rk, x, grid=grid, variant=aes.AES_VAR_HYBRID)
+        assert np.array_equal(pt.cpu().numpy(), want_pt), (keybits, n, grid)
+        y = x.clone()
+        aes.ecb_encrypt(rk, y, out=y, grid=grid, variant=aes.AES_VAR_HYBRID)
+        assert np.array_equal(y.cpu().numpy(), want_ct), ("in place", keybits, n, grid)
+    for grid in (1, 2, 5):   # the bitsliced-only kernel: partial 8-unit groups at every grid size
+        n = 8 * 256 * grid + 129
+        x = _dev_rand(n)
+        want = oracle.encrypt(key, synth.blocks(0, n), nthreads=16)
+        ct = aes.ecb_encrypt(rk, x, grid=grid, variant=aes.AES_VAR_BITSLICE)
+        assert np.array_equal(ct.cpu().numpy(), want), ("bitslice", keybits, n, grid)
 
 
 def test_data_structure_variants(aes):

@@ -1,0 +1,179 @@
+// tools/mb/hyb.cu -- knobs for the hybrid (T-table + bitsliced warps) kernel:
+// how many blocks each side processes, what the T-table side costs with the
+// unit queue, and how the split responds to the number of bitsliced warps.
+// Same building blocks as paper_1902_05234_b200/csrc/aes_hybrid.cu.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "aes_bitslice.cuh"
+#include "aes_device.cuh"
+
+using namespace aesb200;
+
+constexpr uint64_t kUnit = 32, kSuper = 64;
+
+__device__ __forceinline__ uint64_t unit_block(uint32_t u) {
+    const uint64_t sc = (uint64_t)(u / (uint32_t)kSuper) * gridDim.x + blockIdx.x;   // IMAD.WIDE.U32
+    return sc * (kSuper * kUnit) + (u % (uint32_t)kSuper) * kUnit;
+}
+
+template <int NR, bool DEC, class BaseOf>
+__device__ __forceinline__ void bs_pass(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n,
+                                        const BSK& bk, BaseOf base) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t v[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        const uint64_t i = base(j) + lane;
+        uint4 x = make_uint4(0, 0, 0, 0);
+        if (i < n) x = __ldcs(in + i);
+        v[j][0] = x.x; v[j][1] = x.y; v[j][2] = x.z; v[j][3] = x.w;
+    }
+    uint32_t R[4][8];
+    bs_pack(v, R);
+    if (DEC) bs_decrypt<NR>(R, bk);
+    else bs_encrypt<NR>(R, bk);
+    bs_unpack(R, v);
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        const uint64_t i = base(j) + lane;
+        if (i < n) __stcs(out + i, make_uint4(v[j][0], v[j][1], v[j][2], v[j][3]));
+    }
+}
+
+// WT T-table warps; BMODE 0: bitsliced warps work, 1: they exit at once
+template <int WT, int RT, int RB, int BMODE, int TU = 1>
+__global__ void __launch_bounds__(kThreads, 1)
+    hyb(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n, const __grid_constant__ RK rk,
+        const __grid_constant__ BSK bk, unsigned long long* bcount, uint64_t tail_units) {
+    static_assert(WT * RT + (32 - WT) * RB <= 32 * 64, "setmaxnreg.inc would wait forever");
+    static_assert(WT < 32 || BMODE == 1, "no bitsliced warps");
+    extern __shared__ __align__(16) uint32_t smem[];
+    __shared__ uint32_t q_next;
+    if (threadIdx.x == 0) q_next = 0;
+    const Tab<V_REPL> tb = Tab<V_REPL>::template setup<false>(smem);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp < WT) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(RT));
+        if (TU == 1) {
+        // claims run two units ahead: the atomic of unit t+2 is issued before
+        // unit t's rounds and its result is only read (shfl) after them
+        uint32_t a = 0;
+        if (lane == 0) a = atomicAdd(&q_next, 1u);
+        const uint32_t ucur = __shfl_sync(0xffffffffu, a, 0);
+        if (lane == 0) a = atomicAdd(&q_next, 1u);
+        uint32_t unxt = __shfl_sync(0xffffffffu, a, 0);
+        const uint64_t b = unit_block(ucur);
+        if (b >= n) return;
+        uint64_t i = b + lane;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (i < n) v = __ldcs(in + i);
+        for (;;) {
+            const uint64_t nb = unit_block(unxt);
+            const uint64_t ni = nb + lane;
+            uint4 nv = make_uint4(0, 0, 0, 0);
+            if (ni < n) nv = __ldcs(in + ni);
+            if (lane == 0) a = atomicAdd(&q_next, 1u);
+            if (i < n) __stcs(out + i, cipher_block<10, false>(tb, v, rk));
+            if (nb >= n) break;
+            unxt = __shfl_sync(0xffffffffu, a, 0);
+            i = ni;
+            v = nv;
+        }
+        } else {
+        // two units (kSuper is even, so u and u+1 share a super-chunk: blocks b..b+63)
+        uint32_t a = 0;
+        if (lane == 0) a = atomicAdd(&q_next, 2u);
+        const uint32_t ucur = __shfl_sync(0xffffffffu, a, 0);
+        if (lane == 0) a = atomicAdd(&q_next, 2u);
+        uint32_t unxt = __shfl_sync(0xffffffffu, a, 0);
+        const uint64_t b = unit_block(ucur);
+        if (b >= n) return;
+        uint64_t i = b + lane;
+        uint4 v0 = make_uint4(0, 0, 0, 0), v1 = v0;
+        if (i < n) v0 = __ldcs(in + i);
+        if (i + 32 < n) v1 = __ldcs(in + i + 32);
+        for (;;) {
+            const uint64_t nb = unit_block(unxt);
+            const uint64_t ni = nb + lane;
+            uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
+            if (ni < n) n0 = __ldcs(in + ni);
+            if (ni + 32 < n) n1 = __ldcs(in + ni + 32);
+            if (lane == 0) a = atomicAdd(&q_next, 2u);
+            if (i < n) __stcs(out + i, cipher_block<10, false>(tb, v0, rk));
+            if (i + 32 < n) __stcs(out + i + 32, cipher_block<10, false>(tb, v1, rk));
+            if (nb >= n) break;
+            unxt = __shfl_sync(0xffffffffu, a, 0);
+            i = ni;
+            v0 = n0;
+            v1 = n1;
+        }
+        }
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(RB));
+        if (BMODE == 1) return;
+        unsigned long long mine = 0;
+        for (;;) {
+            uint32_t u0 = ~0u;
+            if (lane == 0) {
+                const uint32_t seen = *reinterpret_cast<volatile uint32_t*>(&q_next);
+                if (unit_block(seen + (uint32_t)tail_units) < n) u0 = atomicAdd(&q_next, 8u);
+            }
+            u0 = __shfl_sync(0xffffffffu, u0, 0);
+            if (u0 == ~0u || unit_block(u0) >= n) break;
+            bs_pass<10, false>(in, out, n, bk, [&](int j) { return unit_block(u0 + j); });
+            mine += 256;
+        }
+        if (lane == 0) atomicAdd(bcount, mine);
+    }
+}
+
+template <int WT, int RT, int RB, int BMODE, int TU = 1>
+static float run(const uint4* in, uint4* out, uint64_t n, const RK& rk, const BSK& bk, unsigned long long* cnt,
+                 int grid, uint64_t tail, unsigned long long* hcnt) {
+    const void* f = (const void*)hyb<WT, RT, RB, BMODE, TU>;
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemReplEnc);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int r = 0; r < 5; r++) {
+        cudaMemset(cnt, 0, sizeof *cnt);
+        cudaEventRecord(e0);
+        hyb<WT, RT, RB, BMODE, TU><<<grid, kThreads, kSmemReplEnc>>>(in, out, n, rk, bk, cnt, tail);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r && ms < best) {
+            best = ms;
+            cudaMemcpy(hcnt, cnt, sizeof *cnt, cudaMemcpyDeviceToHost);
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaError_t err = cudaGetLastError();
+    return err == cudaSuccess ? best : -(float)err;
+}
+
+extern "C" int hyb_run(const void* in, void* out, uint64_t n, const uint32_t* ek, int grid, float* ms,
+                       unsigned long long* bblocks, void* scratch) {
+    RK rk;
+    for (int i = 0; i < 60; i++) rk.w[i] = ek[i];
+    static BSK bk;
+    bs_expand_round_keys(ek, 10, bk);
+    auto* cnt = static_cast<unsigned long long*>(scratch);
+    const uint4* pi = static_cast<const uint4*>(in);
+    uint4* po = static_cast<uint4*>(out);
+    int k = 0;
+#define R(WT, RT, RB, BM, TAIL, TU) ms[k] = run<WT, RT, RB, BM, TU>(pi, po, n, rk, bk, cnt, grid, TAIL, &bblocks[k]), k++
+    R(28, 56, 120, 1, 384, 1);    // T warps alone, queue structure
+    R(28, 56, 120, 0, 384, 1);    // hybrid as in the product
+    R(28, 56, 120, 1, 384, 2);    // T alone, 2 units per claim
+    R(28, 56, 120, 0, 384, 2);    // hybrid, 2 units per claim
+    R(32, 64, 64, 1, 384, 1);     // 32 T warps, queue
+    R(32, 64, 64, 1, 384, 2);
+#undef R
+    return k;
+}
