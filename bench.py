@@ -310,18 +310,57 @@ def _e2e(aes, pdist, key, rk, x, ct, pt, nbytes, K, dev):
             "link_frac": (2.0 * nbytes * KE / dt / 1e9) / link}   # bytes each way per second / ceiling
 
 
+HYBRID_MIN_BLOCKS = 1 << 23    # aes_ecb.cu kHybridMinBlocks: the default kernel from here up is the hybrid one
+
+
+def _hybrid_ceiling(dom, clocks, nsm):
+    """Joint shared-memory-data-path + ALU roofline of the hybrid kernel
+    (DESIGN.md 6): per SM per clock the L1 data path moves 32 lane-slots (one
+    conflict-free LDS.32 wavefront; a block's LDG.128 + STG.128 take 8 of them)
+    and the ALU pipe retires 64 lane-ops.  With the per-block instruction counts
+    read from the kernel's SASS (profiles/r02_sass_counts.json, tools/sass_counts.py)
+      T-table block:  L_T lookups + 8 slots,  A_T ALU ops
+      bitsliced block:          8 slots,      A_B ALU ops
+    the most blocks per clock are t + b with 32 = L_T t + 8 (t + b) and
+    64 = A_T t + A_B b (both resources saturated)."""
+    p = os.path.join(ROOT, "profiles", "r02_sass_counts.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p)).get(f"nr{NR}_{'dec' if dom == 'decrypt' else 'enc'}")
+    if not d:
+        return None
+    LT, AT = d["t_table_per_block"]["lds"], d["t_table_per_block"]["alu"]
+    AB = d["bitsliced_per_block"]["alu"]
+    # solve [LT+8, 8; AT, AB] [t; b] = [32; 64]
+    a11, a12, a21, a22 = LT + 8, 8.0, AT, AB
+    det = a11 * a22 - a12 * a21
+    t = (32 * a22 - a12 * 64) / det
+    b = (a11 * 64 - a21 * 32) / det
+    f = (clocks.get("sm_mhz") or 1965.0) * 1e6
+    blocks_per_s = (t + b) * nsm * f
+    return {"bound": "smem_data_path+alu", "peak_blocks_per_clk_per_sm": t + b, "t_share": t / (t + b),
+            "peak_GBps_payload": 16 * blocks_per_s / 1e9, "per_block_ops": {"t_table_lookups": LT, "t_table_alu": AT,
+                                                                            "bitsliced_alu": AB},
+            "source": "profiles/r02_sass_counts.json + nominal 32 LDS lane-slots and 64 ALU lane-ops /clk/SM "
+                      "at the measured SM clock"}
+
+
 def _rooflines(n, enc_ms, dec_ms, lds_peak, nsm, clocks):
-    """roofline (HBM, the BASELINE metric's denominator) and roofline_lds (the
-    binding one) of the dominant kernel, from its event-timed average launch."""
+    """roofline (HBM, the BASELINE metric's denominator), roofline_lds (the
+    T-table ceiling) and roofline_hybrid (the joint LDS + ALU ceiling of the
+    default hybrid kernel) of the dominant kernel, from its event-timed average launch."""
     peak, peak_src, _ = measured_peaks()
     kern_ms = max(enc_ms, dec_ms)
     dom = "encrypt" if enc_ms >= dec_ms else "decrypt"
+    hybrid = n >= HYBRID_MIN_BLOCKS
+    kname = (f"hybrid_kernel<10,{dom}> (aes_ecb_{dom}: 28 T-table + 4 bitsliced warps per CTA)" if hybrid
+             else f"ecb_kernel<10,{dom}> (aes_ecb_{dom})")
     achieved = 32.0 * n / (kern_ms * 1e-3) / 1e9               # GB/s, 16 B read + 16 B written per block
     traffic, traffic_src = ncu_traffic(32 * n)
     lookups = 16 * NR * n
     lds_nominal = nsm * 32 * (clocks.get("sm_mhz") or 1965.0) * 1e6
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": f"ecb_kernel<10,{dom}> (aes_ecb_{dom})", "kernel_ms": kern_ms,
+            "traffic": traffic, "kernel": kname, "kernel_ms": kern_ms,
             "peak_source": peak_src, "algorithmic_bytes_per_launch": 32 * n, "traffic_source": traffic_src}
     rate = lookups / (kern_ms * 1e-3)
     roof_lds = {"bound": "smem_lookup", "achieved": rate / 1e12, "peak": lds_peak / 1e12, "unit": "Tlookup/s",
@@ -329,7 +368,16 @@ def _rooflines(n, enc_ms, dec_ms, lds_peak, nsm, clocks):
                 "peak_source": "aes_mb_lds_gather measured in this run (conflict-free 1-PRMT LDS gathers)",
                 "nominal_peak": lds_nominal / 1e12, "frac_of_nominal": rate / lds_nominal,
                 "lookups_per_launch": lookups}
-    return roof, roof_lds, peak
+    roof_hyb = None
+    if hybrid:
+        roof_lds["equivalent"] = ("16*Nr lookups counted for EVERY block; the bitsliced warps cipher ~10% of the "
+                                  "blocks without any lookup, so this exceeds the T-table-only ceiling (frac > 1 is "
+                                  "the point of the hybrid kernel)")
+        hc = _hybrid_ceiling(dom, clocks, nsm)
+        if hc:
+            got = 16.0 * n / (kern_ms * 1e-3) / 1e9
+            roof_hyb = dict(hc, achieved_GBps_payload=got, frac=got / hc["peak_GBps_payload"])
+    return roof, roof_lds, roof_hyb, peak
 
 
 def run_ours(a):
@@ -441,7 +489,7 @@ def run_ours(a):
     ctr_gbps = 8 * 3 * nbytes / (ev0.elapsed_time(ev1) * 1e-3) / 1e9
 
     e2e = None if a.no_e2e else _e2e(aes, pdist, key, rk, x, ct, pt, nbytes, K, dev)
-    roof, roof_lds, peak = _rooflines(n, enc_ms, dec_ms, lds_peak, nsm, clocks)
+    roof, roof_lds, roof_hyb, peak = _rooflines(n, enc_ms, dec_ms, lds_peak, nsm, clocks)
 
     # per-rank spread: kernel and step times, devices used
     ranks = {"world": world, "backend": pdist.backend_name(),
@@ -473,14 +521,18 @@ def run_ours(a):
                        "step": f"expand_key + encrypt({nbytes / GIB:g} GiB) + decrypt({nbytes / GIB:g} GiB)",
                        "l2": (f"inputs ({nbytes / 2**20:.0f} MiB) larger than L2 ({l2 / 2**20:.0f} MiB); no flush"
                               if nbytes > l2 else "inputs smaller than L2 (harness-test size): L2-warm"),
-                       "variant": "smem_repl, 1 state/thread, persistent grid"},
+                       "variant": ("default = hybrid: 28 T-table warps (lane-replicated smem tables) + 4 bitsliced "
+                                   "warps per 1024-thread CTA, persistent grid" if n >= HYBRID_MIN_BLOCKS else
+                                   "default = smem_repl, 1 state/thread, persistent grid")},
             "GBps": gbps / 8, "enc_ms": enc_ms, "dec_ms": dec_ms,
             "enc_Gbps": 8 * nbytes / (enc_ms * 1e-3) / 1e9, "dec_Gbps": 8 * nbytes / (dec_ms * 1e-3) / 1e9,
             "hbm_frac_step": (32.0 * n * 2 * K / (ms_local * 1e-3) / 1e9) / peak,
-            "roofline": roof, "roofline_lds": roof_lds,
+            "roofline": roof, "roofline_lds": roof_lds, "roofline_hybrid": roof_hyb,
             "roofline_note": ("T-table AES does 16*Nr shared-memory lookups per 32 HBM bytes, so the binding "
-                              "roofline is the shared-memory gather rate (roofline_lds), not HBM; T-table "
-                              "AES-128 ECB cannot exceed ~28% of HBM on B200 (DESIGN.md 6, 11)"),
+                              "roofline is the shared-memory gather rate (roofline_lds), not HBM (T-table AES-128 "
+                              "ECB alone cannot exceed ~28% of HBM on B200); the default hybrid kernel adds "
+                              "lookup-free bitsliced warps on the idle ALU, bounded jointly by the data path and "
+                              "the ALU pipe (roofline_hybrid; DESIGN.md 6, 11)"),
             "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clocks, "gpu_launches": 2 * K, "gpu": torch.cuda.get_device_name(dev),
             "wall_window_ms_rank0": wall_ms, "ranks": ranks,

@@ -154,7 +154,8 @@ aes_status aes_ecb_batch(const aes_round_keys *keys, int nkeys, int decrypt, con
 
 /* Kernel variants (T-table placement).  All variants
  * produce bit-identical output; they differ only in speed.
- *  AES_VAR_DEFAULT    : tuned choice (currently AES_VAR_SMEM_REPL).
+ *  AES_VAR_DEFAULT    : tuned choice: AES_VAR_HYBRID for ECB messages of 2^23
+ *                       blocks (128 MiB) or more, AES_VAR_SMEM_REPL below.
  *  AES_VAR_SMEM_REPL  : Te0..Te3 (Td0..Td3, Si) replicated 32x in shared
  *                       memory, bank == lane, conflict-free by construction.
  *  AES_VAR_SMEM_PLAIN : one copy of each table in shared memory (Li et al.,

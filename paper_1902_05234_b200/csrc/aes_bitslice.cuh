@@ -33,21 +33,49 @@
 
 namespace aesb200 {
 
+// One 3-input LUT (LOP3.LUT, immediate = truth table over a=0xF0, b=0xCC, c=0xAA).
+// The device branch is inline PTX (not a constant expression); constexpr
+// evaluation only ever runs the host branch.
+#pragma nv_diag_suppress 2388
+template <unsigned IMM>
+__host__ __device__ __forceinline__ constexpr uint32_t bs_lop3(uint32_t a, uint32_t b, uint32_t c) {
+#ifdef __CUDA_ARCH__
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(IMM));
+    return d;
+#else
+    uint32_t r = 0;
+    for (int i = 0; i < 8; i++)
+        if (IMM >> i & 1) r |= (i & 4 ? a : ~a) & (i & 2 ? b : ~b) & (i & 1 ? c : ~c);
+    return r;
+#endif
+}
+#pragma nv_diag_default 2388
+
 #include "aes_bs_sbox.inc"
 
 // Bitsliced round keys: k[round][r * 8 + b], rounds 0..NR (encryption: ek;
-// decryption: the equivalent-inverse dk in application order).
+// decryption: the equivalent-inverse dk in application order), and the
+// power-of-two multipliers that move the packing shifts and the ShiftRows
+// rotations onto the FMA pipe (IMAD / IMAD.HI / IMAD.WIDE): passed at run time
+// so ptxas cannot strength-reduce them back to ALU shifts (the ALU pipe is
+// what the bitsliced warps compete for).
 struct BSK {
     uint32_t k[15][32];
+    uint32_t shl[5];     // shl[s] = 2^s           (s = 1, 2, 4): x << s = x * shl[s]
+    uint32_t shr[5];     // shr[s] = 2^(32 - s):  x >> s = hi(x * shr[s])
+    uint32_t rot[4];     // rot[r] = 2^(32 - 8r): rotr(x, 8r) = lo(x * rot[r]) + hi(x * rot[r])
+    uint32_t one;        // 1: the final add of a rotation stays an IMAD
 };
 
-__host__ __device__ constexpr uint32_t bs_rotr(uint32_t x, int n) {
+__host__ __device__ constexpr uint32_t bs_mulhi(uint32_t a, uint32_t b) {
 #ifdef __CUDA_ARCH__
-    return __funnelshift_r(x, x, n);
+    return __umulhi(a, b);
 #else
-    return n ? (x >> n) | (x << (32 - n)) : x;
+    return (uint32_t)(((uint64_t)a * b) >> 32);
 #endif
 }
+
 
 __host__ __device__ constexpr uint32_t bs_perm(uint32_t a, uint32_t b, uint32_t s) {
 #ifdef __CUDA_ARCH__
@@ -60,27 +88,28 @@ __host__ __device__ constexpr uint32_t bs_perm(uint32_t a, uint32_t b, uint32_t 
 #endif
 }
 
-// swap bit (p + s) of a with bit p of b for every p with (p & s) == 0 in its byte
-__host__ __device__ constexpr void bs_swapmove(uint32_t& a, uint32_t& b, uint32_t m, int s) {
-    const uint32_t t = ((a >> s) ^ b) & m;
+// swap bit (p + s) of a with bit p of b for every p with (p & s) == 0 in its
+// byte; the two shifts are IMAD.HI / IMAD (FMA pipe), the rest 3 LOP3
+__host__ __device__ constexpr void bs_swapmove(uint32_t& a, uint32_t& b, uint32_t m, int s, const BSK& bk) {
+    const uint32_t t = (bs_mulhi(a, bk.shr[s]) ^ b) & m;
     b ^= t;
-    a ^= t << s;
+    a ^= t * bk.shl[s];
 }
 
 // 8x8 bit transpose inside each byte lane: bit b of byte r of w[j] <-> bit j of byte r of w[b]
-__host__ __device__ constexpr void bs_transpose8(uint32_t (&w)[8]) {
-    bs_swapmove(w[0], w[1], 0x55555555u, 1);
-    bs_swapmove(w[2], w[3], 0x55555555u, 1);
-    bs_swapmove(w[4], w[5], 0x55555555u, 1);
-    bs_swapmove(w[6], w[7], 0x55555555u, 1);
-    bs_swapmove(w[0], w[2], 0x33333333u, 2);
-    bs_swapmove(w[1], w[3], 0x33333333u, 2);
-    bs_swapmove(w[4], w[6], 0x33333333u, 2);
-    bs_swapmove(w[5], w[7], 0x33333333u, 2);
-    bs_swapmove(w[0], w[4], 0x0F0F0F0Fu, 4);
-    bs_swapmove(w[1], w[5], 0x0F0F0F0Fu, 4);
-    bs_swapmove(w[2], w[6], 0x0F0F0F0Fu, 4);
-    bs_swapmove(w[3], w[7], 0x0F0F0F0Fu, 4);
+__host__ __device__ constexpr void bs_transpose8(uint32_t (&w)[8], const BSK& bk) {
+    bs_swapmove(w[0], w[1], 0x55555555u, 1, bk);
+    bs_swapmove(w[2], w[3], 0x55555555u, 1, bk);
+    bs_swapmove(w[4], w[5], 0x55555555u, 1, bk);
+    bs_swapmove(w[6], w[7], 0x55555555u, 1, bk);
+    bs_swapmove(w[0], w[2], 0x33333333u, 2, bk);
+    bs_swapmove(w[1], w[3], 0x33333333u, 2, bk);
+    bs_swapmove(w[4], w[6], 0x33333333u, 2, bk);
+    bs_swapmove(w[5], w[7], 0x33333333u, 2, bk);
+    bs_swapmove(w[0], w[4], 0x0F0F0F0Fu, 4, bk);
+    bs_swapmove(w[1], w[5], 0x0F0F0F0Fu, 4, bk);
+    bs_swapmove(w[2], w[6], 0x0F0F0F0Fu, 4, bk);
+    bs_swapmove(w[3], w[7], 0x0F0F0F0Fu, 4, bk);
 }
 
 // 4x4 byte transpose: byte c of y[r] = byte r of x[c]
@@ -94,11 +123,11 @@ __host__ __device__ constexpr void bs_transpose4(uint32_t& x0, uint32_t& x1, uin
 }
 
 // v[j][c] = column word c of block j  ->  R[r][b]
-__host__ __device__ constexpr void bs_pack(const uint32_t (&v)[8][4], uint32_t (&R)[4][8]) {
+__host__ __device__ constexpr void bs_pack(const uint32_t (&v)[8][4], uint32_t (&R)[4][8], const BSK& bk) {
     uint32_t X[4][8] = {};
     for (int c = 0; c < 4; c++) {
         uint32_t w[8] = {v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], v[5][c], v[6][c], v[7][c]};
-        bs_transpose8(w);                                  // w[b]: byte r, bit j = bit b of byte r of block j
+        bs_transpose8(w, bk);                              // w[b]: byte r, bit j = bit b of byte r of block j
         for (int b = 0; b < 8; b++) X[c][b] = w[b];
     }
     for (int b = 0; b < 8; b++) {
@@ -107,11 +136,11 @@ __host__ __device__ constexpr void bs_pack(const uint32_t (&v)[8][4], uint32_t (
     }
 }
 
-__host__ __device__ constexpr void bs_unpack(uint32_t (&R)[4][8], uint32_t (&v)[8][4]) {
+__host__ __device__ constexpr void bs_unpack(uint32_t (&R)[4][8], uint32_t (&v)[8][4], const BSK& bk) {
     for (int b = 0; b < 8; b++) bs_transpose4(R[0][b], R[1][b], R[2][b], R[3][b]);   // R[c][b] = old X[c][b]
     for (int c = 0; c < 4; c++) {
         uint32_t w[8] = {R[c][0], R[c][1], R[c][2], R[c][3], R[c][4], R[c][5], R[c][6], R[c][7]};
-        bs_transpose8(w);
+        bs_transpose8(w, bk);
         for (int j = 0; j < 8; j++) v[j][c] = w[j];
     }
 }
@@ -130,15 +159,22 @@ __host__ __device__ constexpr void bs_inv_sub_bytes(uint32_t (&R)[4][8]) {
     for (int r = 0; r < 4; r++) bs_inv_sbox(R[r]);
 }
 
-// ShiftRows (Eq 19): row r, column c <- column c + r  ==  rotate right by 8r
-__host__ __device__ constexpr void bs_shift_rows(uint32_t (&R)[4][8]) {
-    for (int r = 1; r < 4; r++)
-        for (int b = 0; b < 8; b++) R[r][b] = bs_rotr(R[r][b], 8 * r);
+// rotr(x, 8r) on the FMA pipe: IMAD.WIDE.U32 (x * 2^(32-8r) = hi:lo) + IMAD (lo * 1 + hi)
+__host__ __device__ constexpr uint32_t bs_rotr8(uint32_t x, int r, const BSK& bk) {
+    const uint64_t p = (uint64_t)x * bk.rot[r];
+    return (uint32_t)p * bk.one + (uint32_t)(p >> 32);
 }
 
-__host__ __device__ constexpr void bs_inv_shift_rows(uint32_t (&R)[4][8]) {
+// ShiftRows (Eq 19): row r, column c <- column c + r  ==  rotate right by 8r
+__host__ __device__ constexpr void bs_shift_rows(uint32_t (&R)[4][8], const BSK& bk) {
     for (int r = 1; r < 4; r++)
-        for (int b = 0; b < 8; b++) R[r][b] = bs_rotr(R[r][b], 32 - 8 * r);
+        for (int b = 0; b < 8; b++) R[r][b] = bs_rotr8(R[r][b], r, bk);
+}
+
+// InvShiftRows: rotate row r right by 32 - 8r
+__host__ __device__ constexpr void bs_inv_shift_rows(uint32_t (&R)[4][8], const BSK& bk) {
+    for (int r = 1; r < 4; r++)
+        for (int b = 0; b < 8; b++) R[r][b] = bs_rotr8(R[r][b], 4 - r, bk);
 }
 
 // xtime on a bitsliced byte, bit b of the result
@@ -179,6 +215,12 @@ __host__ __device__ constexpr void bs_inv_mix_columns_ark(uint32_t (&R)[4][8], c
 
 // Round keys (host): round i of `w` (4(NR+1) LE column words) -> bk.k[i]
 __host__ __device__ constexpr void bs_expand_round_keys(const uint32_t* w, int nr, BSK& bk) {
+    for (int q = 0; q < 5; q++) {
+        bk.shl[q] = 1u << q;
+        bk.shr[q] = q ? 1u << (32 - q) : 0u;
+    }
+    for (int r = 0; r < 4; r++) bk.rot[r] = r ? 1u << (32 - 8 * r) : 1u;
+    bk.one = 1;
     for (int i = 0; i <= nr; i++)
         for (int r = 0; r < 4; r++)
             for (int b = 0; b < 8; b++) {
@@ -204,11 +246,11 @@ __host__ __device__ constexpr void bs_encrypt(uint32_t (&R)[4][8], const BSK& bk
 #endif
     for (int i = 1; i < NR; i++) {
         bs_sub_bytes(R);
-        bs_shift_rows(R);
+        bs_shift_rows(R, bk);
         bs_mix_columns_ark(R, BSKeyAt{bk, i});
     }
     bs_sub_bytes(R);
-    bs_shift_rows(R);
+    bs_shift_rows(R, bk);
     bs_ark(R, BSKeyAt{bk, NR});
 }
 
@@ -221,11 +263,11 @@ __host__ __device__ constexpr void bs_decrypt(uint32_t (&R)[4][8], const BSK& bk
 #endif
     for (int i = 1; i < NR; i++) {
         bs_inv_sub_bytes(R);
-        bs_inv_shift_rows(R);
+        bs_inv_shift_rows(R, bk);
         bs_inv_mix_columns_ark(R, BSKeyAt{bk, i});
     }
     bs_inv_sub_bytes(R);
-    bs_inv_shift_rows(R);
+    bs_inv_shift_rows(R, bk);
     bs_ark(R, BSKeyAt{bk, NR});
 }
 
@@ -306,10 +348,10 @@ constexpr uint32_t run(bool dec, const uint32_t (&in)[4], int slot, int c) {
     for (int j = 0; j < 8; j++)
         for (int q = 0; q < 4; q++) v[j][q] = j == slot ? in[q] : 0x9E3779B9u * (uint32_t)(4 * j + q + 1);
     uint32_t R[4][8] = {};
-    bs_pack(v, R);
+    bs_pack(v, R, bk);
     if (dec) bs_decrypt<NR>(R, bk);
     else bs_encrypt<NR>(R, bk);
-    bs_unpack(R, v);
+    bs_unpack(R, v, bk);
     return v[slot][c];
 }
 constexpr uint32_t kPt[4] = {0x33221100u, 0x77665544u, 0xBBAA9988u, 0xFFEEDDCCu};

@@ -438,6 +438,8 @@ KernelInfo pick_mode(int nr, int mode) {
     return {f, kSmemReplDec};
 }
 
+constexpr uint64_t kHybridMinBlocks = 1ull << 23;
+
 aes_status launch(const aes_round_keys* rk, int nr, int decrypt, const void* in, void* out, uint64_t nblocks,
                   cudaStream_t stream, const aes_launch_config* cfg, bool check_ptrs, int mode = M_ECB,
                   const ModeP* mp = nullptr) {
@@ -447,7 +449,12 @@ aes_status launch(const aes_round_keys* rk, int nr, int decrypt, const void* in,
     int spt = cfg ? cfg->states_per_thread : 0;
     int grid_req = cfg ? cfg->grid : 0;
     const int flags = cfg ? cfg->flags : 0;
-    if (variant == AES_VAR_DEFAULT) variant = V_REPL;   // measured best
+    // Default: the hybrid kernel (T-table + bitsliced warps) from 2^23 blocks
+    // (128 MiB) up, where its bitsliced warps get enough work to pay for
+    // running 28 instead of 32 T-table warps; the replicated T-table kernel
+    // below that (measured crossover 64-128 MiB).
+    if (variant == AES_VAR_DEFAULT)
+        variant = (mode == M_ECB && spt <= 1 && nblocks >= kHybridMinBlocks) ? V_HYBRID : V_REPL;
     if (spt == 0) spt = 1;                              // S = 1, 2, 4 measure within 1 %
     if (grid_req < 0 || (flags & ~(AES_LAUNCH_TRUSTED_PTRS | AES_LAUNCH_NO_PDL))) return AES_ERANGE;
     if (flags & AES_LAUNCH_TRUSTED_PTRS) check_ptrs = false;

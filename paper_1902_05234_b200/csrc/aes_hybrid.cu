@@ -71,10 +71,10 @@ __device__ __forceinline__ void bs_pass(const uint4* __restrict__ in, uint4* __r
         v[j][0] = x.x; v[j][1] = x.y; v[j][2] = x.z; v[j][3] = x.w;
     }
     uint32_t R[4][8];
-    bs_pack(v, R);
+    bs_pack(v, R, bk);
     if (DEC) bs_decrypt<NR>(R, bk);
     else bs_encrypt<NR>(R, bk);
-    bs_unpack(R, v);
+    bs_unpack(R, v, bk);
 #pragma unroll
     for (int j = 0; j < 8; j++) {
         const uint64_t i = base(j) + lane;

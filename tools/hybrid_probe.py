@@ -41,12 +41,16 @@ def timeit(fn, s, reps=10):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--mib", type=int, default=1024)
+    ap.add_argument("--mib", type=int, nargs="*", default=[1024])
     ap.add_argument("--keybits", type=int, nargs="*", default=[128, 192, 256])
     ap.add_argument("--variants", type=int, nargs="*", default=[1, 7, 8])
     a = ap.parse_args()
     s = torch.cuda.Stream()
-    n = a.mib << 16
+    for mib in a.mib:
+        run_size(a, s, mib << 16)
+
+
+def run_size(a, s, n):
     for kb in a.keybits:
         rk = aes.expand_key(synth.key(kb))
         x = torch.empty(16 * n, dtype=torch.uint8, device="cuda")

@@ -13,6 +13,28 @@ using namespace aesb200;
 
 constexpr uint64_t kUnit = 32, kSuper = 64;
 
+// T-table access with some byte positions addressed on the FMA pipe:
+// FM bit 0: byte 3 (IMAD.HI + IMAD), bit 1: byte 0 (IMAD + IMAD.HI)
+struct Mul {
+    uint32_t m24, m16, m8;
+};
+template <int FM>
+struct TabF {
+    const char* sb;
+    uint32_t lo, m24, m16, m8;
+    __device__ __forceinline__ uint32_t addr(uint32_t s, int k) const {
+        if ((FM & 2) && k == 0) return __umulhi(s * m24, m16) + lo;
+        if ((FM & 1) && k == 3) return __umulhi(s, m8) * m8 + lo;
+        return __byte_perm(lo, s, 0x1140 + 16 * k);
+    }
+    __device__ __forceinline__ uint32_t t(int i, uint32_t s, int k) const {
+        return *reinterpret_cast<const uint32_t*>(sb + aesb200::off_t(i) + addr(s, k));
+    }
+    __device__ __forceinline__ uint32_t si(uint32_t s, int k) const {
+        return *reinterpret_cast<const uint32_t*>(sb + kOffSi + addr(s, k));
+    }
+};
+
 __device__ __forceinline__ uint64_t unit_block(uint32_t u) {
     const uint64_t sc = (uint64_t)(u / (uint32_t)kSuper) * gridDim.x + blockIdx.x;   // IMAD.WIDE.U32
     return sc * (kSuper * kUnit) + (u % (uint32_t)kSuper) * kUnit;
@@ -31,10 +53,10 @@ __device__ __forceinline__ void bs_pass(const uint4* __restrict__ in, uint4* __r
         v[j][0] = x.x; v[j][1] = x.y; v[j][2] = x.z; v[j][3] = x.w;
     }
     uint32_t R[4][8];
-    bs_pack(v, R);
+    bs_pack(v, R, bk);
     if (DEC) bs_decrypt<NR>(R, bk);
     else bs_encrypt<NR>(R, bk);
-    bs_unpack(R, v);
+    bs_unpack(R, v, bk);
 #pragma unroll
     for (int j = 0; j < 8; j++) {
         const uint64_t i = base(j) + lane;
@@ -43,16 +65,17 @@ __device__ __forceinline__ void bs_pass(const uint4* __restrict__ in, uint4* __r
 }
 
 // WT T-table warps; BMODE 0: bitsliced warps work, 1: they exit at once
-template <int WT, int RT, int RB, int BMODE, int TU = 1>
+template <int WT, int RT, int RB, int BMODE, int TU = 1, int FM = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     hyb(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n, const __grid_constant__ RK rk,
-        const __grid_constant__ BSK bk, unsigned long long* bcount, uint64_t tail_units) {
+        const __grid_constant__ BSK bk, unsigned long long* bcount, uint64_t tail_units, const __grid_constant__ Mul mul) {
     static_assert(WT * RT + (32 - WT) * RB <= 32 * 64, "setmaxnreg.inc would wait forever");
     static_assert(WT < 32 || BMODE == 1, "no bitsliced warps");
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ uint32_t q_next;
     if (threadIdx.x == 0) q_next = 0;
-    const Tab<V_REPL> tb = Tab<V_REPL>::template setup<false>(smem);
+    const Tab<V_REPL> tb0 = Tab<V_REPL>::template setup<false>(smem);
+    const TabF<FM> tb{tb0.sb, tb0.lo, mul.m24, mul.m16, mul.m8};
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp < WT) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(RT));
@@ -129,10 +152,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-template <int WT, int RT, int RB, int BMODE, int TU = 1>
+template <int WT, int RT, int RB, int BMODE, int TU = 1, int FM = 0>
 static float run(const uint4* in, uint4* out, uint64_t n, const RK& rk, const BSK& bk, unsigned long long* cnt,
                  int grid, uint64_t tail, unsigned long long* hcnt) {
-    const void* f = (const void*)hyb<WT, RT, RB, BMODE, TU>;
+    const void* f = (const void*)hyb<WT, RT, RB, BMODE, TU, FM>;
+    const Mul mul{1u << 24, 1u << 16, 1u << 8};
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemReplEnc);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
@@ -141,7 +165,7 @@ static float run(const uint4* in, uint4* out, uint64_t n, const RK& rk, const BS
     for (int r = 0; r < 5; r++) {
         cudaMemset(cnt, 0, sizeof *cnt);
         cudaEventRecord(e0);
-        hyb<WT, RT, RB, BMODE, TU><<<grid, kThreads, kSmemReplEnc>>>(in, out, n, rk, bk, cnt, tail);
+        hyb<WT, RT, RB, BMODE, TU, FM><<<grid, kThreads, kSmemReplEnc>>>(in, out, n, rk, bk, cnt, tail, mul);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms = 0;
@@ -167,13 +191,15 @@ extern "C" int hyb_run(const void* in, void* out, uint64_t n, const uint32_t* ek
     const uint4* pi = static_cast<const uint4*>(in);
     uint4* po = static_cast<uint4*>(out);
     int k = 0;
-#define R(WT, RT, RB, BM, TAIL, TU) ms[k] = run<WT, RT, RB, BM, TU>(pi, po, n, rk, bk, cnt, grid, TAIL, &bblocks[k]), k++
-    R(28, 56, 120, 1, 384, 1);    // T warps alone, queue structure
-    R(28, 56, 120, 0, 384, 1);    // hybrid as in the product
-    R(28, 56, 120, 1, 384, 2);    // T alone, 2 units per claim
-    R(28, 56, 120, 0, 384, 2);    // hybrid, 2 units per claim
-    R(32, 64, 64, 1, 384, 1);     // 32 T warps, queue
-    R(32, 64, 64, 1, 384, 2);
+#define R(WT, RT, RB, BM, TAIL, TU, FM) ms[k] = run<WT, RT, RB, BM, TU, FM>(pi, po, n, rk, bk, cnt, grid, TAIL, &bblocks[k]), k++
+    R(28, 56, 120, 1, 384, 2, 0);    // T alone, PRMT addressing
+    R(28, 56, 120, 0, 384, 2, 0);    // hybrid (product)
+    R(28, 56, 120, 1, 384, 2, 1);    // T alone, byte 3 on FMA
+    R(28, 56, 120, 0, 384, 2, 1);    // hybrid, byte 3 on FMA
+    R(28, 56, 120, 1, 384, 2, 2);    // T alone, byte 0 on FMA
+    R(28, 56, 120, 0, 384, 2, 2);    // hybrid, byte 0 on FMA
+    R(28, 56, 120, 0, 384, 2, 3);    // hybrid, bytes 0 and 3 on FMA
+    R(24, 48, 112, 0, 384, 2, 1);    // 24 T + 8 B, byte 3 on FMA
 #undef R
     return k;
 }

@@ -7,7 +7,7 @@ buffer, 1024-thread CTAs x 148), after a parity check of every variant
 against the default kernel (itself oracle-checked in tests/) and the golden
 (oracle-written) samples.  Meant to run under
 
-  ncu --set full --clock-control none -k regex:ecb -o prof_variants \
+  ncu --set full --clock-control none -k regex:'ecb|hybrid|bs_kernel' -o prof_variants \
       python tools/ncu_variants.py
 
 so the capture holds the reference launch (default kernel) and then exactly
@@ -27,7 +27,11 @@ from synth import golden
 
 VARIANTS = [(aes.AES_VAR_SMEM_REPL, "smem_repl (default)"), (aes.AES_VAR_SMEM_REPL_TMA, "smem_repl + TMA staging"),
             (aes.AES_VAR_SMEM_ROT, "one table + rotations"), (aes.AES_VAR_SMEM_PLAIN, "smem_plain (Li et al.)"),
-            (aes.AES_VAR_GLOBAL, "global __ldg (L1)"), (aes.AES_VAR_CONST, "const (the paper's choice)")]
+            (aes.AES_VAR_GLOBAL, "global __ldg (L1)"), (aes.AES_VAR_CONST, "const (the paper's choice)"),
+            (aes.AES_VAR_HYBRID, "hybrid: T-table + bitsliced warps"), (aes.AES_VAR_BITSLICE, "bitsliced only")]
+if os.environ.get("AES_NCU_ONLY"):        # e.g. AES_NCU_ONLY=7,8: just these variants
+    _keep = {int(v) for v in os.environ["AES_NCU_ONLY"].split(",")}
+    VARIANTS = [(v, nm) for v, nm in VARIANTS if v in _keep]
 
 
 def main():
