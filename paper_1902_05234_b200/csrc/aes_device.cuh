@@ -342,4 +342,93 @@ __device__ __forceinline__ uint4 cipher_block(const TB& tb, uint4 v, const RK& r
     return final_round<DEC>(tb, s0, s1, s2, s3, KeyAt{rk, NR});                    // A8
 }
 
+// ---------------------------------------------------------------------------
+// Modes (NEXT-1 CTR, NEXT-4 CBC decryption): parameters and shared pieces
+// ---------------------------------------------------------------------------
+enum { M_ECB = 0, M_CTR = 1, M_CBCD = 2 };
+
+struct ModeP {
+    uint32_t iv[4];    // CBC: IV as LE column words
+    uint64_t ctr_hi;   // CTR: counter of block 0 of this launch, big-endian value,
+    uint64_t ctr_lo;   //      split into high / low 64 bits
+};
+
+__device__ __forceinline__ uint4 counter_block(const ModeP& mp, uint64_t i) {
+    uint64_t lo = mp.ctr_lo + i;
+    uint64_t hi = mp.ctr_hi + (lo < mp.ctr_lo ? 1ull : 0ull);   // carry, wraps mod 2^128
+    // block bytes 0..7 = hi big-endian, 8..15 = lo big-endian; columns are LE words
+    return make_uint4(__byte_perm((uint32_t)(hi >> 32), 0, 0x0123), __byte_perm((uint32_t)hi, 0, 0x0123),
+                      __byte_perm((uint32_t)(lo >> 32), 0, 0x0123), __byte_perm((uint32_t)lo, 0, 0x0123));
+}
+
+__device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
+    return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w);
+}
+
+// CTR with counter-mode caching (Bernstein-Schwabe): the counters of 256
+// consecutive blocks differ only in byte 15 (row 3 of column 3), so in round 1
+// only column 0 depends on it (one Te3 lookup) and in round 2 each column has
+// exactly one varying input byte (four lookups); everything else is a
+// per-256-block-group constant (8 words: P0, e1..e3 of round 1 and Q0..Q3 of
+// round 2), so every block needs 1 + 4 + 16*(NR-3) + 16 lookups instead of
+// 16*NR (133 vs 160 for AES-128).
+constexpr size_t kCtrTableBytes = (kThreads / 32) * 32 * 8 * 4;   // 32 warps x 32 entries x 8 words = 32 KiB
+
+// Group constants (8 words) of the 256-block counter group starting at the
+// 128-bit counter (ghi:glo) with byte 15 = 0.
+template <class TB>
+__device__ __forceinline__ void ctr_group_constants(const TB& tb, const RK& rk, uint64_t ghi, uint64_t glo,
+                                                    uint32_t* dst) {
+    // representative counter (byte 15 = 0), round 0
+    const uint32_t s0 = __byte_perm((uint32_t)(ghi >> 32), 0, 0x0123) ^ rk.w[0];
+    const uint32_t s1 = __byte_perm((uint32_t)ghi, 0, 0x0123) ^ rk.w[1];
+    const uint32_t s2 = __byte_perm((uint32_t)(glo >> 32), 0, 0x0123) ^ rk.w[2];
+    const uint32_t s3 = __byte_perm((uint32_t)glo, 0, 0x0123) ^ rk.w[3];
+    // round 1: e1..e3 do not see byte 15; e0 = P0 ^ Te3[byte 3 of s3]
+    const uint32_t P0 = tb.t(0, s0, 0) ^ tb.t(1, s1, 1) ^ tb.t(2, s2, 2) ^ rk.w[4];
+    const uint32_t e1 = tb.t(0, s1, 0) ^ tb.t(1, s2, 1) ^ tb.t(2, s3, 2) ^ tb.t(3, s0, 3) ^ rk.w[5];
+    const uint32_t e2 = tb.t(0, s2, 0) ^ tb.t(1, s3, 1) ^ tb.t(2, s0, 2) ^ tb.t(3, s1, 3) ^ rk.w[6];
+    const uint32_t e3 = tb.t(0, s3, 0) ^ tb.t(1, s0, 1) ^ tb.t(2, s1, 2) ^ tb.t(3, s2, 3) ^ rk.w[7];
+    // round 2: f_j = Q_j ^ (the one lookup of a byte of e0)
+    const uint32_t Q0 = tb.t(1, e1, 1) ^ tb.t(2, e2, 2) ^ tb.t(3, e3, 3) ^ rk.w[8];
+    const uint32_t Q1 = tb.t(0, e1, 0) ^ tb.t(1, e2, 1) ^ tb.t(2, e3, 2) ^ rk.w[9];
+    const uint32_t Q2 = tb.t(0, e2, 0) ^ tb.t(1, e3, 1) ^ tb.t(3, e1, 3) ^ rk.w[10];
+    const uint32_t Q3 = tb.t(0, e3, 0) ^ tb.t(2, e1, 2) ^ tb.t(3, e2, 3) ^ rk.w[11];
+    uint4* gw = reinterpret_cast<uint4*>(dst);
+    gw[0] = make_uint4(P0, e1, e2, e3);
+    gw[1] = make_uint4(Q0, Q1, Q2, Q3);
+}
+
+
+// Lane `lane` of a warp fills entry `lane` of the warp's 32-entry group table
+// wt: the constants of group (lane & 1) (0: the group holding block tcb, 1: the
+// next one) of the 32-block run starting at block tcb -- the run of trip
+// (lane >> 1) of the warp's next 16.
+template <class TB>
+__device__ __forceinline__ void ctr_fill_group(const TB& tb, const RK& rk, const ModeP& mp, uint64_t tcb,
+                                               uint32_t lane, uint32_t* wt) {
+    const uint64_t lo_c = mp.ctr_lo + tcb;
+    const uint64_t hi_c = mp.ctr_hi + (lo_c < mp.ctr_lo ? 1ull : 0ull);
+    const uint64_t g0 = lo_c & ~0xffull;
+    const uint64_t glo = g0 + 256ull * (lane & 1);
+    ctr_group_constants(tb, rk, hi_c + (glo < g0 ? 1ull : 0ull), glo, wt + 8 * lane);
+}
+
+// Output block cb + lane of a 32-block run (trip `trip` of the table) in CTR
+// mode with the cached group constants: 1 + 4 + 16*(NR-3) + 16 lookups.
+template <int NR, class TB>
+__device__ __forceinline__ uint4 ctr_cached_block(const TB& tb, const RK& rk, const ModeP& mp, const uint32_t* wt,
+                                                  uint32_t trip, uint64_t cb, uint32_t lane, uint4 p) {
+    const uint32_t off = (uint32_t)((mp.ctr_lo + cb) & 0xff) + lane;   // < 256 + 32
+    const uint4* c = reinterpret_cast<const uint4*>(wt + 8 * (2 * trip + (off >> 8)));
+    const uint4 c0 = c[0], c1 = c[1];
+    const uint32_t x = (off & 0xff) ^ (rk.w[3] >> 24);                 // byte 15 of this counter ^ k0
+    const uint32_t e0 = c0.x ^ tb.t(3, x << 24, 3);
+    uint32_t f0 = c1.x ^ tb.t(0, e0, 0), f1 = c1.y ^ tb.t(3, e0, 3);
+    uint32_t f2 = c1.z ^ tb.t(2, e0, 2), f3 = c1.w ^ tb.t(1, e0, 1);
+#pragma unroll
+    for (int r = 3; r < NR; r++) t_round<false>(tb, f0, f1, f2, f3, KeyAt{rk, r});
+    return xor4(p, final_round<false>(tb, f0, f1, f2, f3, KeyAt{rk, NR}));
+}
+
 }  // namespace aesb200

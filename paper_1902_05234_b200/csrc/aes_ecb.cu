@@ -48,26 +48,6 @@ namespace aesb200 {
 //   ctr_kernel          C_i = P_i ^ E(ctr0 + i), BE 128-bit counter  (Eq 5, R24)
 //   cbc_decrypt_kernel  P_i = D(C_i) ^ C_{i-1}, C_{-1} = IV          (Eq 2, R25)
 // ---------------------------------------------------------------------------
-enum { M_ECB = 0, M_CTR = 1, M_CBCD = 2 };
-
-struct ModeP {
-    uint32_t iv[4];    // CBC: IV as LE column words
-    uint64_t ctr_hi;   // CTR: counter of block 0 of this launch, big-endian value,
-    uint64_t ctr_lo;   //      split into high / low 64 bits
-};
-
-__device__ __forceinline__ uint4 counter_block(const ModeP& mp, uint64_t i) {
-    uint64_t lo = mp.ctr_lo + i;
-    uint64_t hi = mp.ctr_hi + (lo < mp.ctr_lo ? 1ull : 0ull);   // carry, wraps mod 2^128
-    // block bytes 0..7 = hi big-endian, 8..15 = lo big-endian; columns are LE words
-    return make_uint4(__byte_perm((uint32_t)(hi >> 32), 0, 0x0123), __byte_perm((uint32_t)hi, 0, 0x0123),
-                      __byte_perm((uint32_t)(lo >> 32), 0, 0x0123), __byte_perm((uint32_t)lo, 0, 0x0123));
-}
-
-__device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
-    return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w);
-}
-
 template <int NR, bool DEC, int V, int SPT, int MODE>
 __device__ __forceinline__ void aes_body(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n,
                                          const RK& rk, const ModeP& mp) {
@@ -155,40 +135,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     aes_body<NR, false, V_REPL, 1, M_CTR>(in, out, n, rk, mp);
 }
 
-// CTR with counter-mode caching (Bernstein-Schwabe): the counters of 256
-// consecutive blocks differ only in byte 15 (row 3 of column 3), so in round 1
-// only column 0 depends on it (one Te3 lookup) and in round 2 each column has
-// exactly one varying input byte (four lookups); everything else is a
-// per-256-block-group constant (8 words: P0, e1..e3 of round 1 and Q0..Q3 of
-// round 2), so every block needs 1 + 4 + 16*(NR-3) + 16 lookups instead of
-// 16*NR (133 vs 160 for AES-128).
-constexpr size_t kCtrTableBytes = (kThreads / 32) * 32 * 8 * 4;   // 32 warps x 32 entries x 8 words = 32 KiB
-
-// Group constants (8 words) of the 256-block counter group starting at the
-// 128-bit counter (ghi:glo) with byte 15 = 0.
-template <class TB>
-__device__ __forceinline__ void ctr_group_constants(const TB& tb, const RK& rk, uint64_t ghi, uint64_t glo,
-                                                    uint32_t* dst) {
-    // representative counter (byte 15 = 0), round 0
-    const uint32_t s0 = __byte_perm((uint32_t)(ghi >> 32), 0, 0x0123) ^ rk.w[0];
-    const uint32_t s1 = __byte_perm((uint32_t)ghi, 0, 0x0123) ^ rk.w[1];
-    const uint32_t s2 = __byte_perm((uint32_t)(glo >> 32), 0, 0x0123) ^ rk.w[2];
-    const uint32_t s3 = __byte_perm((uint32_t)glo, 0, 0x0123) ^ rk.w[3];
-    // round 1: e1..e3 do not see byte 15; e0 = P0 ^ Te3[byte 3 of s3]
-    const uint32_t P0 = tb.t(0, s0, 0) ^ tb.t(1, s1, 1) ^ tb.t(2, s2, 2) ^ rk.w[4];
-    const uint32_t e1 = tb.t(0, s1, 0) ^ tb.t(1, s2, 1) ^ tb.t(2, s3, 2) ^ tb.t(3, s0, 3) ^ rk.w[5];
-    const uint32_t e2 = tb.t(0, s2, 0) ^ tb.t(1, s3, 1) ^ tb.t(2, s0, 2) ^ tb.t(3, s1, 3) ^ rk.w[6];
-    const uint32_t e3 = tb.t(0, s3, 0) ^ tb.t(1, s0, 1) ^ tb.t(2, s1, 2) ^ tb.t(3, s2, 3) ^ rk.w[7];
-    // round 2: f_j = Q_j ^ (the one lookup of a byte of e0)
-    const uint32_t Q0 = tb.t(1, e1, 1) ^ tb.t(2, e2, 2) ^ tb.t(3, e3, 3) ^ rk.w[8];
-    const uint32_t Q1 = tb.t(0, e1, 0) ^ tb.t(1, e2, 1) ^ tb.t(2, e3, 2) ^ rk.w[9];
-    const uint32_t Q2 = tb.t(0, e2, 0) ^ tb.t(1, e3, 1) ^ tb.t(3, e1, 3) ^ rk.w[10];
-    const uint32_t Q3 = tb.t(0, e3, 0) ^ tb.t(2, e1, 2) ^ tb.t(3, e2, 3) ^ rk.w[11];
-    uint4* gw = reinterpret_cast<uint4*>(dst);
-    gw[0] = make_uint4(P0, e1, e2, e3);
-    gw[1] = make_uint4(Q0, Q1, Q2, Q3);
-}
-
 template <int NR>
 __global__ void __launch_bounds__(kThreads, 1)
     ctr_cached_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n,
@@ -211,29 +157,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if ((t & 15) == 0) {
             __syncwarp();                    // previous 16 trips' entries fully read
             const uint64_t tcb = cb + (uint64_t)(lane >> 1) * T;
-            if (tcb < n) {
-                const uint64_t lo_c = mp.ctr_lo + tcb;
-                const uint64_t hi_c = mp.ctr_hi + (lo_c < mp.ctr_lo ? 1ull : 0ull);
-                const uint64_t g0 = lo_c & ~0xffull;
-                const uint64_t glo = g0 + 256ull * (lane & 1);
-                ctr_group_constants(tb, rk, hi_c + (glo < g0 ? 1ull : 0ull), glo, wt + 8 * lane);
-            }
+            if (tcb < n) ctr_fill_group(tb, rk, mp, tcb, lane, wt);
             __syncwarp();
         }
         const uint64_t i = cb + lane;
-        if (i < n) {
-            const uint4 p = __ldcs(in + i);
-            const uint32_t off = (uint32_t)((mp.ctr_lo + cb) & 0xff) + lane;   // < 256 + 32
-            const uint4* c = reinterpret_cast<const uint4*>(wt + 8 * (2 * (uint32_t)(t & 15) + (off >> 8)));
-            const uint4 c0 = c[0], c1 = c[1];
-            const uint32_t x = (off & 0xff) ^ (rk.w[3] >> 24);                 // byte 15 of this counter ^ k0
-            const uint32_t e0 = c0.x ^ tb.t(3, x << 24, 3);
-            uint32_t f0 = c1.x ^ tb.t(0, e0, 0), f1 = c1.y ^ tb.t(3, e0, 3);
-            uint32_t f2 = c1.z ^ tb.t(2, e0, 2), f3 = c1.w ^ tb.t(1, e0, 1);
-#pragma unroll
-            for (int r = 3; r < NR; r++) t_round<false>(tb, f0, f1, f2, f3, KeyAt{rk, r});
-            __stcs(out + i, xor4(p, final_round<false>(tb, f0, f1, f2, f3, KeyAt{rk, NR})));
-        }
+        if (i < n) __stcs(out + i, ctr_cached_block<NR>(tb, rk, mp, wt, (uint32_t)(t & 15), cb, lane, __ldcs(in + i)));
     }
 }
 
@@ -416,15 +344,19 @@ KernelInfo pick(int nr, bool dec, int v, int spt) {
     return {nullptr, 0};
 }
 
+// AES_B200_CTR_KERNEL=plain selects the uncached T-table CTR kernel (A/B measurement only)
+bool ctr_plain_requested() {
+    static const bool plain = [] {
+        const char* e = std::getenv("AES_B200_CTR_KERNEL");
+        return e && std::strcmp(e, "plain") == 0;
+    }();
+    return plain;
+}
+
 KernelInfo pick_mode(int nr, int mode) {
     const void* f = nullptr;
     if (mode == M_CTR) {
-        // AES_B200_CTR_KERNEL=plain selects the uncached kernel (A/B measurement only)
-        static const bool plain = [] {
-            const char* e = std::getenv("AES_B200_CTR_KERNEL");
-            return e && std::strcmp(e, "plain") == 0;
-        }();
-        if (plain) {
+        if (ctr_plain_requested()) {
             f = nr == 10 ? (const void*)&ctr_kernel<10> : nr == 12 ? (const void*)&ctr_kernel<12>
                                                                    : (const void*)&ctr_kernel<14>;
             return {f, kSmemReplEnc};
@@ -440,6 +372,13 @@ KernelInfo pick_mode(int nr, int mode) {
 
 constexpr uint64_t kHybridMinBlocks = 1ull << 23;
 
+// AES_B200_HYBRID_MIN_BLOCKS=<n> moves the default-kernel crossover (tests use
+// it to put the hybrid CTR / CBC kernels under small oracle-checked inputs).
+uint64_t hybrid_min_blocks() {
+    const char* e = std::getenv("AES_B200_HYBRID_MIN_BLOCKS");
+    return e ? std::strtoull(e, nullptr, 10) : kHybridMinBlocks;
+}
+
 aes_status launch(const aes_round_keys* rk, int nr, int decrypt, const void* in, void* out, uint64_t nblocks,
                   cudaStream_t stream, const aes_launch_config* cfg, bool check_ptrs, int mode = M_ECB,
                   const ModeP* mp = nullptr) {
@@ -454,13 +393,16 @@ aes_status launch(const aes_round_keys* rk, int nr, int decrypt, const void* in,
     // running 28 instead of 32 T-table warps; the replicated T-table kernel
     // below that (measured crossover 64-128 MiB).
     if (variant == AES_VAR_DEFAULT)
-        variant = (mode == M_ECB && spt <= 1 && nblocks >= kHybridMinBlocks) ? V_HYBRID : V_REPL;
+        variant = (spt <= 1 && nblocks >= hybrid_min_blocks() && !(mode == M_CTR && ctr_plain_requested()))
+                      ? V_HYBRID
+                      : V_REPL;
     if (spt == 0) spt = 1;                              // S = 1, 2, 4 measure within 1 %
     if (grid_req < 0 || (flags & ~(AES_LAUNCH_TRUSTED_PTRS | AES_LAUNCH_NO_PDL))) return AES_ERANGE;
     if (flags & AES_LAUNCH_TRUSTED_PTRS) check_ptrs = false;
-    bool bsk = mode == M_ECB && (variant == V_HYBRID || variant == V_BITSLICE);
-    KernelInfo ki = mode != M_ECB ? pick_mode(nr, mode)
-                    : bsk         ? (spt == 1 ? pick_hybrid(nr, decrypt != 0, variant) : KernelInfo{nullptr, 0})
+    if (mode != M_ECB && variant != V_HYBRID) variant = V_REPL;   // the modes: hybrid or their own kernels
+    bool bsk = variant == V_HYBRID || variant == V_BITSLICE;
+    KernelInfo ki = bsk           ? (spt == 1 ? pick_hybrid(nr, decrypt != 0, variant, mode) : KernelInfo{nullptr, 0})
+                    : mode != M_ECB ? pick_mode(nr, mode)
                                   : pick(nr, decrypt != 0, variant, spt);
     if (mode != M_ECB) spt = 1;
     if (!ki.fn) return AES_EVARIANT;
@@ -486,9 +428,9 @@ aes_status launch(const aes_round_keys* rk, int nr, int decrypt, const void* in,
     unsigned grid = (unsigned)(want < cap ? want : cap);
     if (bsk && variant == V_HYBRID && (nblocks / 32) / grid >= (1ull << 31) - 64) {
         // beyond the hybrid kernel's 32-bit per-CTA unit counter (2^36 blocks per
-        // CTA = 1 TiB): the T-table kernel computes the identical result
+        // CTA = 1 TiB): the T-table kernels compute the identical result
         bsk = false;
-        ki = pick(nr, decrypt != 0, V_REPL, 1);
+        ki = mode != M_ECB ? pick_mode(nr, mode) : pick(nr, decrypt != 0, V_REPL, 1);
         if ((st = resident_ctas(dev, ki, &occ, &nsm))) return st;
     }
     RK k;
@@ -496,11 +438,12 @@ aes_status launch(const aes_round_keys* rk, int nr, int decrypt, const void* in,
     const uint4* pin = static_cast<const uint4*>(in);
     uint4* pout = static_cast<uint4*>(out);
     ModeP m = mp ? *mp : ModeP{};
-    void* args[] = {(void*)&pin, (void*)&pout, (void*)&nblocks, (void*)&k, (void*)&m};
-    if (bsk) {   // hybrid / bitsliced kernels take the bitsliced round keys instead of ModeP
+    void* args[] = {(void*)&pin, (void*)&pout, (void*)&nblocks, (void*)&k, (void*)&m, nullptr};
+    if (bsk) {   // hybrid / bitsliced kernels: (in, out, n, RK, BSK, ModeP)
         static thread_local BSK bs;
         bitslice_keys(rk, decrypt, &bs);
         args[4] = (void*)&bs;
+        args[5] = (void*)&m;
     }
     return launch_kernel(ki, grid, args, stream, !(flags & AES_LAUNCH_NO_PDL));
 }

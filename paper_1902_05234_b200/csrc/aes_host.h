@@ -27,9 +27,9 @@ aes_status stage_h2d(int dev, void* dst, const void* src, size_t bytes, cudaStre
 aes_status validate_keys(const aes_round_keys* rk, int nr);
 aes_status validate_buffers(const void* in, const void* out, uint64_t nblocks);
 aes_status check_device_ptr(const void* p, int dev);
-// Hybrid / bitsliced ECB kernels (aes_hybrid.cu): kernel args (in, out, n, RK, BSK)
+// Hybrid / bitsliced kernels (aes_hybrid.cu): kernel args (in, out, n, RK, BSK, ModeP)
 struct BSK;
-KernelInfo pick_hybrid(int nr, bool dec, int variant);      // variant: V_HYBRID or V_BITSLICE
+KernelInfo pick_hybrid(int nr, bool dec, int variant, int mode);   // V_HYBRID (any mode) or V_BITSLICE (ECB)
 void bitslice_keys(const aes_round_keys* rk, int decrypt, BSK* out);
 // ECB launch used by the host pipeline (aes_ecb.cu)
 aes_status launch_ecb(const aes_round_keys* rk, int nr, int decrypt, const void* in, void* out, uint64_t nblocks,

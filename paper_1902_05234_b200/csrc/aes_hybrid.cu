@@ -11,6 +11,9 @@
 //                           split adapts to whatever rate each side reaches.
 //   bs_kernel<NR,DEC>       AES_VAR_BITSLICE: every warp bitsliced (the ALU-only
 //                           reference point of the ablation).
+// The hybrid kernel also serves the NEXT modes (MODE = M_CTR: the T-table
+// warps keep ctr_cached_kernel's counter-mode caching, claiming 16 units at a
+// time; M_CBCD: P_i = D(C_i) ^ C_{i-1} on both sides).
 //
 // Work order.  CTA c walks its "virtual" unit sequence u = 0, 1, 2, ...;
 // unit u is the 32-block run starting at block
@@ -56,18 +59,22 @@ __device__ __forceinline__ uint64_t unit_block(uint32_t u) {
     return sc * (kSuper * kUnit) + (u % (uint32_t)kSuper) * kUnit;
 }
 
-// One bitsliced pass over 8 x 32 blocks: lane L ciphers blocks base[j] + L.
+// One bitsliced pass over 8 x 32 blocks: lane L handles blocks base(j) + L.
 // Every load/store instruction of the warp moves 512 contiguous bytes.
-template <int NR, bool DEC, class BaseOf>
+//   ECB : out = E/D(in)
+//   CTR : out = in ^ E(counter(i))          (counters computed, Eq 5 / R24)
+//   CBCD: out = D(in) ^ in[i-1] (IV at 0)   (Eq 2 decryption / R25)
+template <int NR, bool DEC, int MODE, class BaseOf>
 __device__ __forceinline__ void bs_pass(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n,
-                                        const BSK& bk, BaseOf base) {
+                                        const BSK& bk, const ModeP& mp, BaseOf base) {
     const uint32_t lane = threadIdx.x & 31;
     uint32_t v[8][4];
 #pragma unroll
     for (int j = 0; j < 8; j++) {
         const uint64_t i = base(j) + lane;
         uint4 x = make_uint4(0, 0, 0, 0);
-        if (i < n) x = __ldcs(in + i);
+        if (MODE == M_CTR) x = counter_block(mp, i);
+        else if (i < n) x = MODE == M_CBCD ? __ldg(in + i) : __ldcs(in + i);
         v[j][0] = x.x; v[j][1] = x.y; v[j][2] = x.z; v[j][3] = x.w;
     }
     uint32_t R[4][8];
@@ -78,14 +85,19 @@ __device__ __forceinline__ void bs_pass(const uint4* __restrict__ in, uint4* __r
 #pragma unroll
     for (int j = 0; j < 8; j++) {
         const uint64_t i = base(j) + lane;
-        if (i < n) __stcs(out + i, make_uint4(v[j][0], v[j][1], v[j][2], v[j][3]));
+        if (i < n) {
+            uint4 y = make_uint4(v[j][0], v[j][1], v[j][2], v[j][3]);
+            if (MODE == M_CTR) y = xor4(y, __ldcs(in + i));
+            if (MODE == M_CBCD) y = xor4(y, i ? __ldg(in + i - 1) : make_uint4(mp.iv[0], mp.iv[1], mp.iv[2], mp.iv[3]));
+            __stcs(out + i, y);
+        }
     }
 }
 
-template <int NR, bool DEC>
+template <int NR, bool DEC, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     hybrid_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n, const __grid_constant__ RK rk,
-                  const __grid_constant__ BSK bk) {
+                  const __grid_constant__ BSK bk, const __grid_constant__ ModeP mp) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ uint32_t q_next;   // next unclaimed unit of this CTA (32-bit: native ATOMS.ADD)
     pdl_launch_dependents();
@@ -95,6 +107,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp < kHybT) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegT));
+        if (MODE == M_CTR) {
+            // Counter-mode caching as in ctr_cached_kernel: a warp claims 16
+            // units, its 32 lanes fill the group constants of their (<= 2)
+            // counter groups into the warp's table, then it walks the units.
+            uint32_t* wt = smem + kSmemReplEnc / 4 + warp * 256;
+            for (;;) {
+                uint32_t a = 0;
+                if (lane == 0) a = atomicAdd(&q_next, 16u);
+                const uint32_t u0 = __shfl_sync(0xffffffffu, a, 0);
+                if (unit_block(u0) >= n) break;
+                __syncwarp();                               // previous claim's entries fully read
+                const uint64_t tcb = unit_block(u0 + (lane >> 1));
+                if (tcb < n) ctr_fill_group(tb, rk, mp, tcb, lane, wt);
+                __syncwarp();
+#pragma unroll 1
+                for (uint32_t t = 0; t < 16; t++) {
+                    const uint64_t cb = unit_block(u0 + t);
+                    if (cb >= n) break;
+                    const uint64_t i = cb + lane;
+                    if (i < n) __stcs(out + i, ctr_cached_block<NR>(tb, rk, mp, wt, t, cb, lane, __ldcs(in + i)));
+                }
+            }
+            return;
+        }
+        // ECB / CBC decryption: one state per lane and unit
+        auto t_in = [&](uint64_t i) { return MODE == M_CBCD ? __ldg(in + i) : __ldcs(in + i); };
+        auto t_out = [&](uint64_t i, uint4 v) {
+            uint4 y = cipher_block<NR, DEC>(tb, v, rk);
+            if (MODE == M_CBCD) y = xor4(y, i ? __ldg(in + i - 1) : make_uint4(mp.iv[0], mp.iv[1], mp.iv[2], mp.iv[3]));
+            return y;
+        };
         // Two units (blocks b .. b+63: kSuper is even) per claim, claimed one
         // step ahead: the atomic for step t+2 is issued before step t's rounds
         // and its result is read (shfl) only after them, so its latency hides.
@@ -107,17 +150,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (b >= n) return;
         uint64_t i = b + lane;
         uint4 v0 = make_uint4(0, 0, 0, 0), v1 = v0;
-        if (i < n) v0 = __ldcs(in + i);
-        if (i + kUnit < n) v1 = __ldcs(in + i + kUnit);
+        if (i < n) v0 = t_in(i);
+        if (i + kUnit < n) v1 = t_in(i + kUnit);
         for (;;) {                          // the next step's states load during this step's rounds
             const uint64_t nb = unit_block(unxt);
             const uint64_t ni = nb + lane;
             uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
-            if (ni < n) n0 = __ldcs(in + ni);
-            if (ni + kUnit < n) n1 = __ldcs(in + ni + kUnit);
+            if (ni < n) n0 = t_in(ni);
+            if (ni + kUnit < n) n1 = t_in(ni + kUnit);
             if (lane == 0) a = atomicAdd(&q_next, 2u);
-            if (i < n) __stcs(out + i, cipher_block<NR, DEC>(tb, v0, rk));
-            if (i + kUnit < n) __stcs(out + i + kUnit, cipher_block<NR, DEC>(tb, v1, rk));
+            if (i < n) __stcs(out + i, t_out(i, v0));
+            if (i + kUnit < n) __stcs(out + i + kUnit, t_out(i + kUnit, v1));
             if (nb >= n) break;
             unxt = __shfl_sync(0xffffffffu, a, 0);
             i = ni;
@@ -134,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             u0 = __shfl_sync(0xffffffffu, u0, 0);
             if (u0 == ~0u || unit_block(u0) >= n) break;
-            bs_pass<NR, DEC>(in, out, n, bk, [&](int j) { return unit_block(u0 + j); });
+            bs_pass<NR, DEC, MODE>(in, out, n, bk, mp, [&](int j) { return unit_block(u0 + j); });
         }
     }
 }
@@ -144,7 +187,7 @@ constexpr int kBsWarps = 16;
 template <int NR, bool DEC>
 __global__ void __launch_bounds__(kThreads, 1)
     bs_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n, const __grid_constant__ RK,
-              const __grid_constant__ BSK bk) {
+              const __grid_constant__ BSK bk, const __grid_constant__ ModeP mp) {
     pdl_launch_dependents();
     pdl_wait();
     // half the warps of the CTA take all registers (16 x 104 + 16 x 24 = 32 x 64)
@@ -156,20 +199,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     // warp-granular grid stride over groups of 256 blocks (8 units)
     const uint64_t warps = (uint64_t)gridDim.x * kBsWarps;
     for (uint64_t g = (uint64_t)blockIdx.x * kBsWarps + (threadIdx.x >> 5); g * 256 < n; g += warps)
-        bs_pass<NR, DEC>(in, out, n, bk, [&](int j) { return g * 256 + (uint64_t)j * 32; });
+        bs_pass<NR, DEC, M_ECB>(in, out, n, bk, mp, [&](int j) { return g * 256 + (uint64_t)j * 32; });
 }
 
 template <int NR, bool DEC>
-KernelInfo hk(int v) {
-    if (v == V_HYBRID) return {reinterpret_cast<const void*>(&hybrid_kernel<NR, DEC>), DEC ? kSmemReplDec : kSmemReplEnc};
-    return {reinterpret_cast<const void*>(&bs_kernel<NR, DEC>), 0};
+KernelInfo hk(int v, int mode) {
+    if (v == V_BITSLICE) return {reinterpret_cast<const void*>(&bs_kernel<NR, DEC>), 0};
+    if (mode == M_CTR) return {reinterpret_cast<const void*>(&hybrid_kernel<NR, false, M_CTR>), kSmemReplEnc + kCtrTableBytes};
+    if (mode == M_CBCD) return {reinterpret_cast<const void*>(&hybrid_kernel<NR, true, M_CBCD>), kSmemReplDec};
+    return {reinterpret_cast<const void*>(&hybrid_kernel<NR, DEC, M_ECB>), DEC ? kSmemReplDec : kSmemReplEnc};
 }
 
-KernelInfo pick_hybrid(int nr, bool dec, int v) {
+KernelInfo pick_hybrid(int nr, bool dec, int v, int mode) {
     switch (nr) {
-        case 10: return dec ? hk<10, true>(v) : hk<10, false>(v);
-        case 12: return dec ? hk<12, true>(v) : hk<12, false>(v);
-        case 14: return dec ? hk<14, true>(v) : hk<14, false>(v);
+        case 10: return dec ? hk<10, true>(v, mode) : hk<10, false>(v, mode);
+        case 12: return dec ? hk<12, true>(v, mode) : hk<12, false>(v, mode);
+        case 14: return dec ? hk<14, true>(v, mode) : hk<14, false>(v, mode);
     }
     return {nullptr, 0};
 }

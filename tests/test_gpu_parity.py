@@ -124,6 +124,45 @@ def test_hybrid_both_paths_against_oracle(aes, keybits):
         assert np.array_equal(ct.cpu().numpy(), want), ("bitslice", keybits, n, grid)
 
 
+def _cbc_decrypt_oracle(key, iv, ct, parts=16):
+    """oracle.cbc decryption in independent chunks (chunk k's IV is the last
+    ciphertext block of chunk k-1), run on host threads (ctypes drops the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+    n = ct.size // 16
+    cuts = [n * k // parts for k in range(parts + 1)]
+    cb = ct.reshape(-1, 16)
+
+    def one(k):
+        a, b = cuts[k], cuts[k + 1]
+        v = iv if a == 0 else cb[a - 1].tobytes()
+        return oracle.cbc(key, v, cb[a:b].reshape(-1).copy(), decrypt=True)
+    with ThreadPoolExecutor(parts) as ex:
+        return np.concatenate(list(ex.map(one, range(parts))))
+
+
+@pytest.mark.parametrize("keybits", [128, 256])
+def test_hybrid_ctr_and_cbc_against_oracle(aes, keybits, monkeypatch):
+    """The NEXT modes on the hybrid kernel (T-table warps with counter-mode
+    caching / CBC chaining + bitsliced warps).  The crossover knob puts the
+    hybrid under a 3M-block input (~640 units per CTA, so the bitsliced warps
+    take part), checked on every block against the oracle."""
+    monkeypatch.setenv("AES_B200_HYBRID_MIN_BLOCKS", "0")
+    key = synth.key(keybits)
+    rk = aes.expand_key(key)
+    n = 3 * 2**20 + 12345
+    x = _dev_rand(n, first=11)
+    host = synth.blocks(11, n)
+    iv = bytes(8) + bytes([0xFF] * 7) + bytes([0xF0])          # low counter half wraps inside the buffer
+    for off in (0, 2**64 - 2**20):
+        got = aes.ctr_xcrypt(rk, iv, x, block_offset=off).cpu().numpy()
+        want = oracle.ctr(key, iv, host, block_offset=off, nthreads=16)
+        assert np.array_equal(got, want), ("ctr", keybits, off, int(np.argmax(got != want)) // 16)
+    civ = bytes(range(16))
+    got = aes.cbc_decrypt(rk, civ, x).cpu().numpy()
+    want = _cbc_decrypt_oracle(key, civ, host)
+    assert np.array_equal(got, want), ("cbc", keybits, int(np.argmax(got != want)) // 16)
+
+
 def test_data_structure_variants(aes):
     key = synth.key(128)
     rk = aes.expand_key(key)
