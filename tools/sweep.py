@@ -34,6 +34,25 @@ import synth
 from synth import golden
 
 NR = {128: 10, 192: 12, 256: 14}
+HYBRID_MIN_BLOCKS = 1 << 23   # aes_ecb.cu: the default kernel is the hybrid one from here up
+
+
+def kernel_of(n, variant=0):
+    if variant == 7 or (variant == 0 and n >= HYBRID_MIN_BLOCKS):
+        return "hybrid"
+    return {8: "bitslice"}.get(variant, "t_table")
+
+
+def lds_fields(lookups_per_block, n, t, ldsp, kernel):
+    """Lookup-rate fraction of the measured LDS-gather ceiling.  For the hybrid
+    kernel 'lookups' are dense-equivalent (every block counted with the T-table
+    lookups although the bitsliced warps cipher some blocks without any), so the
+    fraction can exceed 1."""
+    f = lookups_per_block * n / t / ldsp
+    if kernel == "t_table":
+        return {"lds_frac": f}
+    return {"lds_equiv_frac": f, "lds_note": "dense-equivalent lookups (bitsliced warps do part of the blocks "
+                                              "without lookups): > 1 means beyond the T-table-only ceiling"}
 
 
 def peaks():
@@ -195,7 +214,8 @@ def sizes(a, s, hbm, ldsp):
                        t_call_min_s=tmin, t_call_med_s=tmed, t_device_min_s=dmin, t_device_med_s=dmed,
                        t_graph_b2b_s=tb2b, t_host_call_s=thost, Gbps=g, GBps=g / 8,
                        Gbps_graph_b2b=8 * nbytes / tb2b / 1e9,
-                       hbm_frac=32 * n / dmin / 1e9 / hbm, lds_frac=16 * NR[kb] * n / dmin / ldsp,
+                       hbm_frac=32 * n / dmin / 1e9 / hbm, kernel=kernel_of(n),
+                       **lds_fields(16 * NR[kb], n, dmin, ldsp, kernel_of(n)),
                        l2="flushed" if not warm else "input>2xL2",
                        note="t_call: events around one call incl. host enqueue; t_device: one launch queued "
                             "behind a GPU spin (device time of an isolated launch, L2 flushed if small); "
@@ -222,11 +242,11 @@ def variants(a, s, hbm, ldsp):
     key = synth.key(128)
     rk = aes.expand_key(key)
     names = {1: "smem_repl", 2: "smem_plain", 3: "const (paper)", 4: "smem_repl + TMA staging", 5: "one table + rotations",
-             6: "global __ldg (L1)"}
+             6: "global __ldg (L1)", 7: "hybrid (T-table + bitsliced warps)", 8: "bitsliced only"}
     for kind in ("random", "zeros", "repeat", "ascii"):
         synth.fill_device(x, kind=kind)
-        for v, spt in ((1, 1), (1, 2), (1, 4), (4, 1), (5, 1), (2, 1), (6, 1), (3, 1)):
-            if kind != "random" and (v == 1 and spt != 1 or v in (4, 5)):
+        for v, spt in ((1, 1), (1, 2), (1, 4), (4, 1), (5, 1), (2, 1), (6, 1), (3, 1), (7, 1), (8, 1)):
+            if kind != "random" and (v == 1 and spt != 1 or v in (4, 5, 8)):
                 continue
             for dec in (False, True):
                 f = (lambda: aes.ecb(rk, x, dec, out=out, variant=v, states_per_thread=spt))
@@ -241,7 +261,7 @@ def variants(a, s, hbm, ldsp):
                 g = 8 * nbytes / tmin / 1e9
                 record(what="variant", variant=names[v], spt=spt, data=kind, dir="dec" if dec else "enc",
                        keybits=128, bytes=nbytes, t_min_s=tmin, t_med_s=tmed, Gbps=g,
-                       hbm_frac=32 * n / tmin / 1e9 / hbm, lds_frac=160 * n / tmin / ldsp)
+                       hbm_frac=32 * n / tmin / 1e9 / hbm, **lds_fields(160, n, tmin, ldsp, kernel_of(n, v)))
 
 
 def config3(a, s, hbm, ldsp):
@@ -264,7 +284,7 @@ def config3(a, s, hbm, ldsp):
     n = nbytes // 16
     g = 8 * nbytes / tmin / 1e9
     record(what="config3", keybits=256, dir="dec", bytes=nbytes, t_min_s=tmin, t_med_s=tmed, Gbps=g,
-           hbm_frac=32 * n / tmin / 1e9 / hbm, lds_frac=224 * n / tmin / ldsp)
+           hbm_frac=32 * n / tmin / 1e9 / hbm, kernel=kernel_of(n), **lds_fields(224, n, tmin, ldsp, kernel_of(n)))
 
 
 def ladder(a, s, hbm, ldsp):
@@ -315,25 +335,32 @@ def modes(a, s, hbm, ldsp):
                 f = (lambda: aes.ctr_xcrypt(rk, iv, x, out=out))
             else:
                 f = (lambda: aes.cbc_decrypt(rk, iv, x, out=out))
-            f()
-            torch.cuda.synchronize()
-            parity(kb, out, "ctr" if mode == "ctr" else "cbc_dec")
-            for _ in range(3):
-                f()
-            torch.cuda.synchronize()   # warm-ups ran on the default stream; s is non-blocking
-            tmin, tmed = time_op(f, s, 10)
-            g = 8 * nbytes / tmin / 1e9
-            # the method's own work: CTR with counter-mode caching does 16(Nr-2)+5 lookups per
-            # block plus 27 per warp per 16 trips for its group tables (27/512 per block);
-            # CBC decryption moves 32 DRAM bytes per block (the neighbour block re-read
-            # hits L1/L2) while requesting 48
-            looks = 16 * (NR[kb] - 2) + 5 + 27 / 512 if mode == "ctr" else 16 * NR[kb]
-            record(what="mode", mode=mode, keybits=kb, bytes=nbytes, t_min_s=tmin, t_med_s=tmed, Gbps=g,
-                   hbm_frac=32 * n / tmin / 1e9 / hbm,
-                   requested_bytes_per_block=48 if mode == "cbc_dec" else 32,
-                   lookups_per_block=looks, lds_frac=looks * n / tmin / ldsp,
-                   note="hbm_frac counts 32 DRAM bytes per block (16 read + 16 written); lds_frac counts the "
-                        "lookups this kernel performs")
+            # default kernel (hybrid at 1 GiB), then the T-table-only kernel of the mode
+            for kern, knob in (("hybrid", None), ("t_table", str(1 << 62))):
+                if knob:
+                    os.environ["AES_B200_HYBRID_MIN_BLOCKS"] = knob
+                try:
+                    f()
+                    torch.cuda.synchronize()
+                    parity(kb, out, "ctr" if mode == "ctr" else "cbc_dec")
+                    for _ in range(3):
+                        f()
+                    torch.cuda.synchronize()   # warm-ups ran on the default stream; s is non-blocking
+                    tmin, tmed = time_op(f, s, 10)
+                finally:
+                    os.environ.pop("AES_B200_HYBRID_MIN_BLOCKS", None)
+                g = 8 * nbytes / tmin / 1e9
+                # the method's own work: CTR with counter-mode caching does 16(Nr-2)+5 lookups per
+                # block plus 27 per warp per 16 trips for its group tables (27/512 per block);
+                # CBC decryption moves 32 DRAM bytes per block (the neighbour block re-read
+                # hits L1/L2) while requesting 48
+                looks = 16 * (NR[kb] - 2) + 5 + 27 / 512 if mode == "ctr" else 16 * NR[kb]
+                record(what="mode", mode=mode, kernel=kern, keybits=kb, bytes=nbytes, t_min_s=tmin, t_med_s=tmed,
+                       Gbps=g, hbm_frac=32 * n / tmin / 1e9 / hbm,
+                       requested_bytes_per_block=48 if mode == "cbc_dec" else 32,
+                       lookups_per_block=looks, **lds_fields(looks, n, tmin, ldsp, kern),
+                       note="hbm_frac counts 32 DRAM bytes per block (16 read + 16 written); lookups count "
+                            "the T-table work of this mode")
 
 
 def batch(a, s, hbm, ldsp):
