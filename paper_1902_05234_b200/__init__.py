@@ -302,13 +302,34 @@ def ecb_batch_offsets(rks, in_base: int, out_base: int, in_offsets, out_offsets,
     _check(code, "aes_ecb_batch")
 
 
+def _check_batch_overlap(ip, op, nbytes):
+    """Outputs must be pairwise disjoint, and an output may overlap an input
+    only when it IS that message's own input (in place).  O(m log m)."""
+    import numpy as np
+    i0, o0, ln = (np.asarray(v, dtype=np.uint64) for v in (ip, op, nbytes))
+    order = np.argsort(o0, kind="stable")
+    so, se = o0[order], o0[order] + ln[order]
+    if len(so) > 1 and np.any(so[1:] < se[:-1]):
+        raise ValueError("aes_ecb_batch: output buffers of two messages overlap")
+    # for every input, the output with the largest start below the input's end
+    k = np.searchsorted(so, i0 + ln, side="left").astype(np.int64) - 1
+    hit = k >= 0
+    kk = np.where(hit, k, 0)
+    hit &= se[kk] > i0                                          # that output overlaps the input
+    own = order[kk] == np.arange(len(i0))                       # ... and is the message's own output
+    exact = so[kk] == i0
+    if np.any(hit & ~(own & exact)):
+        raise ValueError("aes_ecb_batch: an output overlaps another message's input (or its own, partially)")
+
+
 def ecb_batch(rks, xs, outs=None, key_index=None, decrypt: bool = False, stream=None):
     """aes_ecb_batch: ECB of many messages (each its own key) in ONE launch.
 
     rks: list of RoundKeys (same key size); xs: list of contiguous CUDA uint8
     tensors on one device (numel % 16 == 0, 16-byte aligned); key_index[i]
     picks rks for xs[i] (default: i).  Returns the list of outputs (``outs``
-    if given; an output may be its own input)."""
+    if given; an output may be its own input, but must not overlap any other
+    message's input or output: ValueError)."""
     import torch
     n = len(xs)
     if key_index is None:
@@ -332,6 +353,7 @@ def ecb_batch(rks, xs, outs=None, key_index=None, decrypt: bool = False, stream=
         return outs
     ip = [xs[i].data_ptr() for i in live]
     op = [outs[i].data_ptr() for i in live]
+    _check_batch_overlap(ip, op, [xs[i].numel() for i in live])
     ib, ob = min(ip), min(op)
     ecb_batch_offsets(rks, ib, ob, [p - ib for p in ip], [p - ob for p in op], [xs[i].numel() // 16 for i in live],
                       [key_index[i] for i in live], decrypt, xs[live[0]].device, stream)

@@ -225,3 +225,15 @@ def test_python_binding_mirrors_abi_names():
                  "aes_ecb_batch", "aes_ecb_trace", "aes_mb_lds_gather"):
         assert callable(getattr(aes, name)), name
     assert aes.aes_expand_key(bytes(16)).ek[:4] == [0, 0, 0, 0]
+
+
+def test_batch_overlap_rules_host_side():
+    """ecb_batch's O(m log m) overlap check: outputs pairwise
+    disjoint; an output may overlap only its own input, exactly (in place)."""
+    from paper_1902_05234_b200 import _check_batch_overlap as check
+    check([0, 256], [0, 256], [256, 256])                       # both in place
+    check([0, 0], [256, 512], [256, 256])                       # shared input
+    check([0, 4096], [8192, 12288], [256, 256])                 # disjoint
+    for ip, op in (([0, 256], [512, 512]), ([0, 256], [256, 512]), ([0], [16]), ([0, 1024], [1024, 0])):
+        with pytest.raises(ValueError):
+            check(ip, op, [256] * len(ip))

@@ -500,6 +500,21 @@ def test_batch_many_messages_many_keys_against_oracle(aes, keybits, decrypt):
         assert np.array_equal(g.cpu().numpy(), want), (i, sizes[i])
 
 
+def test_batch_rejects_overlapping_messages(aes):
+    rk = [aes.expand_key(synth.key(128))]
+    buf = _dev_rand(64)
+    a, b, c = buf[:256], buf[256:512], buf[512:768]
+    outs = aes.ecb_batch(rk * 2, [a, b], outs=[a, b], key_index=[0, 0])      # each in place: fine
+    assert outs[0].data_ptr() == a.data_ptr()
+    with pytest.raises(ValueError):
+        aes.ecb_batch(rk * 2, [a, b], outs=[c, c], key_index=[0, 0])          # two outputs on one buffer
+    with pytest.raises(ValueError):
+        aes.ecb_batch(rk * 2, [a, b], outs=[b, c], key_index=[0, 0])          # output = another input
+    with pytest.raises(ValueError):
+        aes.ecb_batch(rk, [a], outs=[buf[16:272]], key_index=[0])             # partial self-overlap
+    aes.ecb_batch(rk * 2, [a, a], outs=[b, c], key_index=[0, 0])              # shared input: fine
+
+
 def test_batch_thousand_small_files_one_launch(aes):
     key = synth.key(128)
     rk = aes.expand_key(key)
