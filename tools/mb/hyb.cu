@@ -192,14 +192,12 @@ extern "C" int hyb_run(const void* in, void* out, uint64_t n, const uint32_t* ek
     uint4* po = static_cast<uint4*>(out);
     int k = 0;
 #define R(WT, RT, RB, BM, TAIL, TU, FM) ms[k] = run<WT, RT, RB, BM, TU, FM>(pi, po, n, rk, bk, cnt, grid, TAIL, &bblocks[k]), k++
-    R(28, 56, 120, 1, 384, 2, 0);    // T alone, PRMT addressing
+    R(28, 56, 120, 1, 384, 2, 0);    // T alone, 28 warps
     R(28, 56, 120, 0, 384, 2, 0);    // hybrid (product)
-    R(28, 56, 120, 1, 384, 2, 1);    // T alone, byte 3 on FMA
-    R(28, 56, 120, 0, 384, 2, 1);    // hybrid, byte 3 on FMA
-    R(28, 56, 120, 1, 384, 2, 2);    // T alone, byte 0 on FMA
-    R(28, 56, 120, 0, 384, 2, 2);    // hybrid, byte 0 on FMA
-    R(28, 56, 120, 0, 384, 2, 3);    // hybrid, bytes 0 and 3 on FMA
-    R(24, 48, 112, 0, 384, 2, 1);    // 24 T + 8 B, byte 3 on FMA
+    R(24, 48, 112, 1, 384, 2, 0);    // T alone, 24 warps, 48 regs
+    R(24, 48, 112, 0, 384, 2, 0);    // 24 T + 8 B
+    R(24, 56, 88, 0, 384, 2, 0);     // 24 T + 8 B, B at 88 regs
+    R(20, 48, 88, 0, 384, 2, 0);     // 20 T + 12 B
 #undef R
     return k;
 }

@@ -38,8 +38,8 @@ ms = (ctypes.c_float * 16)()
 bb = (ctypes.c_ulonglong * 16)()
 k = L.hyb_run(x.data_ptr(), y.data_ptr(), n, ctypes.cast(ek, ctypes.c_void_p), nsm, ms, bb, scratch.data_ptr())
 torch.cuda.synchronize()
-names = ["T28 alone, PRMT addr", "T28+B4 hybrid, PRMT addr", "T28 alone, byte3 FMA", "T28+B4, byte3 FMA",
-         "T28 alone, byte0 FMA", "T28+B4, byte0 FMA", "T28+B4, bytes 0+3 FMA", "T24+B8, byte3 FMA"]
+names = ["T28 alone", "T28+B4 hybrid", "T24 alone (48 regs)", "T24+B8 (48/112 regs)", "T24+B8 (56/88 regs)",
+         "T20+B12 (48/88 regs)"]
 for i in range(k):
     print(json.dumps({"cfg": names[i], "ms": ms[i], "GBps": 16 * n / (ms[i] * 1e-3) / 1e9,
                       "b_blocks_frac": bb[i] / n}))
