@@ -1,7 +1,8 @@
-// aes_hybrid.cu -- ECB kernels that add bitsliced (lookup-free) warps to the
-// T-table rounds (VERDICT r01 "next" 7; SURVEY.md 7 hard part 1).
+// aes_hybrid.cu -- kernels that add bitsliced (lookup-free) warps to the
+// T-table rounds (VERDICT r01 "next" 7; SURVEY.md 7 hard part 1, R26).
 //
-//   hybrid_kernel<NR,DEC>   AES_VAR_HYBRID: per 1024-thread CTA, kHybT warps run
+//   hybrid_kernel<NR,DEC,MODE>  AES_VAR_HYBRID (the default from 2^23 blocks):
+//                           per 1024-thread CTA, kHybT warps run
 //                           the T-table rounds (Eq 26, the
 //                           production t_round/final_round, lane-replicated
 //                           tables) and kHybB warps run the bitsliced cipher of
@@ -22,7 +23,8 @@
 // CTAs sweep HBM together, as the grid-stride loop of ecb_kernel does) and
 // inside its super-chunk a CTA's warps take units in claim order.  The map is
 // increasing in u, so the first unit at or past n ends a warp's loop.
-// A T-table warp claims 2 units (two blocks per lane); a bitsliced warp claims 8
+// A T-table warp claims 2 units (two blocks per lane; 16 in CTR mode, one
+// counter-group table fill per claim); a bitsliced warp claims 8
 // (eight blocks per lane, unit j -> block slot j) and stops claiming once
 // fewer than kTailUnits units of its CTA remain, so the slow bitsliced claims
 // never form the kernel's tail.
