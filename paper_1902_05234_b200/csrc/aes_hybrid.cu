@@ -148,26 +148,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ucur = __shfl_sync(0xffffffffu, a, 0);
         if (lane == 0) a = atomicAdd(&q_next, 2u);
         uint32_t unxt = __shfl_sync(0xffffffffu, a, 0);
-        const uint64_t b = unit_block(ucur);
+        uint64_t b = unit_block(ucur);
         if (b >= n) return;
-        uint64_t i = b + lane;
-        uint4 v0 = make_uint4(0, 0, 0, 0), v1 = v0;
-        if (i < n) v0 = t_in(i);
-        if (i + kUnit < n) v1 = t_in(i + kUnit);
-        for (;;) {                          // the next step's states load during this step's rounds
-            const uint64_t nb = unit_block(unxt);
-            const uint64_t ni = nb + lane;
-            uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
-            if (ni < n) n0 = t_in(ni);
-            if (ni + kUnit < n) n1 = t_in(ni + kUnit);
-            if (lane == 0) a = atomicAdd(&q_next, 2u);
-            if (i < n) __stcs(out + i, t_out(i, v0));
-            if (i + kUnit < n) __stcs(out + i + kUnit, t_out(i + kUnit, v1));
-            if (nb >= n) break;
-            unxt = __shfl_sync(0xffffffffu, a, 0);
-            i = ni;
-            v0 = n0;
-            v1 = n1;
+        if (b + 2 * kUnit <= n) {
+            // whole steps: no per-lane bounds checks (the unit sequence is
+            // increasing, so once a step is not whole every later one is past n)
+            uint4 v0 = t_in(b + lane), v1 = t_in(b + kUnit + lane);
+            for (;;) {                      // the next step's states load during this step's rounds
+                const uint64_t nb = unit_block(unxt);
+                if (nb + 2 * kUnit > n) {
+                    __stcs(out + b + lane, t_out(b + lane, v0));
+                    __stcs(out + b + kUnit + lane, t_out(b + kUnit + lane, v1));
+                    b = nb;
+                    break;
+                }
+                const uint4 n0 = t_in(nb + lane), n1 = t_in(nb + kUnit + lane);
+                if (lane == 0) a = atomicAdd(&q_next, 2u);
+                __stcs(out + b + lane, t_out(b + lane, v0));
+                __stcs(out + b + kUnit + lane, t_out(b + kUnit + lane, v1));
+                unxt = __shfl_sync(0xffffffffu, a, 0);
+                b = nb;
+                v0 = n0;
+                v1 = n1;
+            }
+        }
+        if (b < n) {                        // the one partial step (ragged end of the message)
+            const uint64_t i = b + lane;
+            if (i < n) __stcs(out + i, t_out(i, t_in(i)));
+            if (i + kUnit < n) __stcs(out + i + kUnit, t_out(i + kUnit, t_in(i + kUnit)));
         }
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegB));

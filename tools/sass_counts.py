@@ -31,7 +31,7 @@ def functions(sass):
 
 def instrs(body):
     return [(int(m.group(1), 16), re.sub(r"^@!?U?P\w+\s+", "", m.group(2)), m.group(0))
-            for m in re.finditer(r"/\*([0-9a-f]{4})\*/\s+((?:@!?U?P\w+\s+)?[A-Z0-9_.]+)[^\n]*", body)]
+            for m in re.finditer(r"/\*([0-9a-f]{4,})\*/\s+((?:@!?U?P\w+\s+)?[A-Z0-9_.]+)[^\n]*", body)]
 
 
 def loops(ins):
@@ -68,7 +68,7 @@ def main():
     res = {"source": "cuobjdump -sass paper_1902_05234_b200/libaes_b200.so (tools/sass_counts.py)",
            "note": "per 16-byte block; ALU = alu-pipe ops, FMA = fma-pipe ops (IMAD*), LDS = lookups (LDS + LDS.U8)"}
     for name, body in functions(sass).items():
-        m = re.search(r"hybrid_kernelILi(\d+)ELb([01])E", name)
+        m = re.search(r"hybrid_kernelILi(\d+)ELb([01])ELi0E", name)   # MODE 0 = ECB
         if not m:
             continue
         nr, dec = int(m.group(1)), m.group(2) == "1"
