@@ -4,6 +4,7 @@
     (pinned), and each direction alone;
   * aes_pipeline_run (encrypt, 1 GiB, pinned in/out) over chunk sizes and depths.
 Parity of every pipeline configuration is checked against the device path."""
+import ctypes
 import json
 import os
 import sys
@@ -44,6 +45,30 @@ for _ in range(2):
 h2d = min(t_copy(False) for _ in range(3))
 both = min(t_copy(True) for _ in range(3))
 print(json.dumps({"what": "copy_ceiling", "h2d_GBps": G / h2d / 1e9, "bidir_GBps_each": G / both / 1e9}))
+# zero copy at full size: one kernel reads and writes the pinned (UVA-mapped)
+# host buffers over the link directly (AES_LAUNCH_TRUSTED_PTRS: the ABI's
+# device-pointer check would refuse host memory), T-table and hybrid kernels
+from paper_1902_05234_b200 import _native  # noqa: E402
+for v, name in ((aes.AES_VAR_SMEM_REPL, "t_table"), (aes.AES_VAR_HYBRID, "hybrid")):
+    cfg = _native.aes_launch_config(v, 0, 0, aes.AES_LAUNCH_TRUSTED_PTRS)
+    sp = torch.cuda.current_stream().cuda_stream
+    def zc():
+        code = _native.lib.aes_ecb_launch(rk.c_ref, rk.nr, 0, hx.data_ptr(), ho.data_ptr(), G // 16, sp,
+                                          ctypes.byref(cfg))
+        assert code == 0, code
+    import ctypes  # noqa: E402
+    ho.zero_()
+    zc()
+    torch.cuda.synchronize()
+    ok = torch.equal(ho, ref)
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        zc()
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    print(json.dumps({"what": "zero_copy", "kernel": name, "ok": ok, "t_s": min(ts), "GBps": G / min(ts) / 1e9,
+                      "Gbps": 8 * G / min(ts) / 1e9}), flush=True)
 for chunk_mb in (8, 32, 64, 128, 256):
     for depth in (2, 3, 4, 6, 8):
         p = aes.Pipeline(chunk_bytes=chunk_mb << 20, depth=depth)
