@@ -83,8 +83,11 @@ def _reduce(value: float, op, device=None) -> float:
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return float(value)
-    t = torch.tensor([float(value)], dtype=torch.float64,
-                     device=device if dist.get_backend() == "nccl" else "cpu")
+    if dist.get_backend() == "nccl":      # NCCL reduces device tensors only
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    else:
+        dev = "cpu"
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=op)
     return float(t.item())
 
