@@ -2,8 +2,10 @@
  * usable without Python or torch.  Part 1 (always): aes_expand_key against
  * FIPS-197 App A.1 and the error codes decided before any CUDA call.
  * Part 2 (argv[1] == "gpu"): the FIPS-197 App C vectors encrypted and
- * decrypted on the device with cudaMalloc'd buffers and a user stream, plus
- * CTR (SP 800-38A F.5.1 block 1), all through the ABI.  Exit 0 = pass. */
+ * decrypted on the device with cudaMalloc'd buffers and a user stream (the
+ * T-table, hybrid and bitsliced kernels), a 128 MiB round trip on the default
+ * (hybrid) kernel, plus CTR (SP 800-38A F.5.1 block 1), all through the ABI.
+ * Exit 0 = pass. */
 #include <stdio.h>
 #include <string.h>
 #include <cuda_runtime.h>
@@ -58,6 +60,55 @@ int main(int argc, char **argv) {
         CHECK(memcmp(ct, want, 16) == 0);
         CHECK(memcmp(back, pt, 16) == 0);
     }
+    /* the same App C vectors through aes_ecb_launch with the hybrid and the
+       bitsliced-only kernels (AES_VAR_HYBRID / AES_VAR_BITSLICE) */
+    for (int v = AES_VAR_HYBRID; v <= AES_VAR_BITSLICE; v++) {
+        aes_launch_config cfg = {v, 0, 0, 0};
+        for (int k = 0; k < 3; k++) {
+            int kb = 128 + 64 * k;
+            hex2bin(kat[k][0], key, kb / 8);
+            hex2bin(kat[k][1], want, 16);
+            CHECK(aes_expand_key(key, kb, &rk) == AES_OK);
+            CHECK(cudaMemcpy(d_in, pt, 16, cudaMemcpyHostToDevice) == cudaSuccess);
+            CHECK(aes_ecb_launch(&rk, rk.nr, 0, d_in, d_out, 1, st, &cfg) == AES_OK);
+            CHECK(aes_ecb_launch(&rk, rk.nr, 1, d_out, d_in, 1, st, &cfg) == AES_OK);
+            CHECK(cudaStreamSynchronize(st) == cudaSuccess);
+            CHECK(cudaMemcpy(ct, d_out, 16, cudaMemcpyDeviceToHost) == cudaSuccess);
+            CHECK(cudaMemcpy(back, d_in, 16, cudaMemcpyDeviceToHost) == cudaSuccess);
+            CHECK(memcmp(ct, want, 16) == 0);
+            CHECK(memcmp(back, pt, 16) == 0);
+        }
+    }
+    /* a message past the hybrid crossover (2^23 blocks, 128 MiB): the default
+       entry points take the hybrid kernel; decrypt(encrypt(x)) == x, and block
+       5 of an all-App-C-plaintext buffer encrypts to the App C ciphertext */
+    {
+        const unsigned long long nb = 1ull << 23;
+        void *big = NULL, *big2 = NULL;
+        CHECK(cudaMalloc(&big, nb * 16) == cudaSuccess && cudaMalloc(&big2, nb * 16) == cudaSuccess);
+        for (unsigned long long j = 0; j < 64; j++)
+            CHECK(cudaMemcpy((char *)big + 16 * j, pt, 16, cudaMemcpyHostToDevice) == cudaSuccess);
+        CHECK(cudaMemset((char *)big + 1024, 0x5a, nb * 16 - 1024) == cudaSuccess);
+        hex2bin(kat[0][0], key, 16);
+        hex2bin(kat[0][1], want, 16);
+        CHECK(aes_expand_key(key, 128, &rk) == AES_OK);
+        CHECK(aes_ecb_encrypt(&rk, rk.nr, big, big2, nb, st) == AES_OK);
+        CHECK(cudaMemcpyAsync(ct, (char *)big2 + 16 * 5, 16, cudaMemcpyDeviceToHost, st) == cudaSuccess);
+        CHECK(aes_ecb_decrypt(&rk, rk.nr, big2, big2, nb, st) == AES_OK);   /* in place */
+        CHECK(cudaStreamSynchronize(st) == cudaSuccess);
+        CHECK(memcmp(ct, want, 16) == 0);
+        static unsigned char h1[4096], h2[4096];
+        for (unsigned long long off = 0; off < nb * 16; off += (nb * 16) / 7 - 16) {
+            unsigned long long o = off & ~15ull;
+            if (o + sizeof h1 > nb * 16) o = nb * 16 - sizeof h1;
+            CHECK(cudaMemcpy(h1, (char *)big + o, sizeof h1, cudaMemcpyDeviceToHost) == cudaSuccess);
+            CHECK(cudaMemcpy(h2, (char *)big2 + o, sizeof h2, cudaMemcpyDeviceToHost) == cudaSuccess);
+            CHECK(memcmp(h1, h2, sizeof h1) == 0);
+        }
+        cudaFree(big); cudaFree(big2);
+    }
+    hex2bin("000102030405060708090a0b0c0d0e0f", key, 16);
+    CHECK(aes_expand_key(key, 128, &rk) == AES_OK);
     /* host pointers are rejected: no CPU fallback */
     CHECK(aes_ecb_encrypt(&rk, rk.nr, pt, ct, 1, st) == AES_ENOTDEVICE);
     /* CTR, SP 800-38A F.5.1 block 1 */
