@@ -7,6 +7,9 @@ A STEP = one pass of the whole hot path over one
 batch: aes_expand_key (host) -> aes_ecb_encrypt(1 GiB) -> aes_ecb_decrypt of
 that ciphertext (1 GiB).  Payload per step and rank = 2 GiB.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--keybits 128|192|256] [--dir both|enc|dec] [--variant NAME] [--spt S] [--seed X]
+(SURVEY.md 5 "Config / flags"; the defaults are BASELINE config 2 -- any other
+setting relabels metric and workload accordingly.)
 For N > 1: one rank per GPU (NCCL only for barrier and the MAX/SUM of
 scalars -- no data-path collective).  Under torchrun
 (--nproc-per-node N) the ranks come from the env; without torchrun the
@@ -34,6 +37,22 @@ METRIC = "AES-128 ECB encrypt/decrypt Gbps at 1/2/4/8 B200; % of HBM roofline"
 WORKLOAD = "AES-128 ECB encrypt and decrypt, 1 GiB random buffer, 1 B200"
 KEYBITS = 128
 NR = 10
+DIR = "both"            # both: encrypt + decrypt per step (BASELINE); enc / dec: one direction
+VARIANT = "default"     # aes_variant by name
+SPT = 0                 # states per thread (0 = default)
+SEED = None             # data seed (None = synth.DATA_SEED, the golden samples' stream)
+VARIANTS = {"default": 0, "smem_repl": 1, "smem_plain": 2, "const": 3, "smem_repl_tma": 4, "smem_rot": 5,
+            "global": 6, "hybrid": 7, "bitslice": 8}
+
+
+def configure(a):
+    """Apply --keybits/--dir/--variant/--spt/--seed (module-level, once per process)."""
+    global KEYBITS, NR, METRIC, WORKLOAD, DIR, VARIANT, SPT, SEED
+    KEYBITS, NR, DIR, VARIANT, SPT, SEED = a.keybits, a.keybits // 32 + 6, a.dir, a.variant, a.spt, a.seed
+    what = {"both": "encrypt/decrypt", "enc": "encrypt", "dec": "decrypt"}[DIR]
+    what2 = {"both": "encrypt and decrypt", "enc": "encrypt", "dec": "decrypt"}[DIR]
+    METRIC = METRIC.replace("AES-128", f"AES-{KEYBITS}").replace("encrypt/decrypt", what)
+    WORKLOAD = WORKLOAD.replace("AES-128", f"AES-{KEYBITS}").replace("encrypt and decrypt", what2)
 
 
 def parse():
@@ -47,7 +66,14 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample length for cpu_baseline")
     ap.add_argument("--ref-seconds", type=float, default=0.0, help="oracle seconds per --impl reference step (0 = auto)")
-    return ap.parse_args()
+    ap.add_argument("--keybits", type=int, default=128, choices=[128, 192, 256])
+    ap.add_argument("--dir", default="both", choices=["both", "enc", "dec"])
+    ap.add_argument("--variant", default="default", choices=sorted(VARIANTS))
+    ap.add_argument("--spt", type=int, default=0, choices=[0, 1, 2, 4], help="states per thread (0 = default)")
+    ap.add_argument("--seed", type=int, default=None, help="data seed (default: synth.DATA_SEED)")
+    a = ap.parse_args()
+    configure(a)
+    return a
 
 
 def host_cores():
@@ -77,21 +103,29 @@ def time_oracle(target_s: float, cores: int):
     import oracle
     import synth
     key = synth.key(KEYBITS)
+    seed = synth.DATA_SEED if SEED is None else SEED
+    passes = 2 if DIR == "both" else 1
+
+    def run(buf):
+        if DIR in ("both", "enc"):
+            buf = oracle.encrypt(key, buf, nthreads=cores)
+        if DIR in ("both", "dec"):
+            oracle.decrypt(key, buf, nthreads=cores)
+
     probe = 4096 * max(1, cores)
-    buf = synth.blocks(0, probe)
+    buf = synth.blocks(0, probe, seed=seed)
     t0 = time.perf_counter()
-    ct = oracle.encrypt(key, buf, nthreads=cores)
-    oracle.decrypt(key, ct, nthreads=cores)
+    run(buf)
     dt = time.perf_counter() - t0
-    rate = 2 * buf.size / dt                       # payload B/s, enc+dec
-    nb = int(min(GIB, max(probe * 16, rate * target_s / 2)) // 16)
-    buf = synth.blocks(0, nb)
+    rate = passes * buf.size / dt                  # payload B/s
+    nb = int(min(GIB, max(probe * 16, rate * target_s / passes)) // 16)
+    buf = synth.blocks(0, nb, seed=seed)
     t0 = time.perf_counter()
-    ct = oracle.encrypt(key, buf, nthreads=cores)
-    oracle.decrypt(key, ct, nthreads=cores)
+    run(buf)
     dt = time.perf_counter() - t0
-    gbps = 8 * 2 * buf.size / dt / 1e9
-    return gbps, f"first {nb} blocks ({buf.size / 2**20:.1f} MiB) of the bench stream, encrypt+decrypt", dt
+    gbps = 8 * passes * buf.size / dt / 1e9
+    what = {"both": "encrypt+decrypt", "enc": "encrypt", "dec": "decrypt"}[DIR]
+    return gbps, f"first {nb} blocks ({buf.size / 2**20:.1f} MiB) of the bench stream, {what}", dt
 
 
 def run_reference(a):
@@ -113,7 +147,7 @@ def run_reference(a):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "Gbps", "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * secs / a.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic (splitmix64 stream, seed 190205234)",
+        "data": f"synthetic (splitmix64 stream, seed {190205234 if SEED is None else SEED})",
         "config": {"workload": WORKLOAD, "keybits": KEYBITS, "sample": sample},
         "cpu_baseline": {"value": v, "unit": "Gbps", "cores": cores, "kind": "oracle", "sample": sample,
                          "cpu": cpu_model()},
@@ -223,15 +257,33 @@ def ncu_traffic(alg_bytes):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def _kernel_kw():
+    """aes.ecb keyword arguments for --variant / --spt (none for the defaults)."""
+    if VARIANT == "default" and SPT == 0:
+        return {}
+    return {"variant": VARIANTS[VARIANT], "states_per_thread": SPT}
+
+
 def _parity_gate(aes, golden, rk, x, ct, pt, s, first, n, dev, rank):
     """No timing record without parity.  Expected values at
     sampled global block indices come from tests/golden/samples.txt (written by
     the oracle, tests/golden/make_samples.py); the oracle itself only runs in
-    the cpu_baseline / reference legs.  Returns True on success."""
+    the cpu_baseline / reference legs.  The check runs on the bench's own
+    buffer in the bench's kernel configuration; with --seed (a stream the
+    samples do not cover) it runs on a same-size buffer of the sampled stream
+    instead, and the bench buffer gets the D(E(x)) == x round trip.  Returns
+    True on success."""
     import torch
+    import synth
+    kw = _kernel_kw()
+    g = x
+    if SEED is not None and SEED != synth.DATA_SEED:
+        g = torch.empty_like(x)
+        with torch.cuda.stream(s):
+            synth.fill_device(g, first_block=first)
     with torch.cuda.stream(s):
-        aes.ecb_encrypt(rk, x, out=ct)
-        aes.ecb_decrypt(rk, ct, out=pt)
+        aes.ecb(rk, x, False, out=ct, **kw)
+        aes.ecb(rk, ct, True, out=pt, **kw)
     s.synchronize()
 
     def gather(t):
@@ -239,9 +291,13 @@ def _parity_gate(aes, golden, rk, x, ct, pt, s, first, n, dev, rank):
 
     try:
         ok = bool(torch.equal(pt, x))                                     # D(E(x)) == x on the whole shard
+        if g is not x:
+            with torch.cuda.stream(s):
+                aes.ecb(rk, g, False, out=ct, **kw)
+            s.synchronize()
         checked = golden.check("ecb_enc", KEYBITS, first, n, gather(ct))  # E(x_i) vs oracle samples
         with torch.cuda.stream(s):
-            aes.ecb_decrypt(rk, x, out=pt)                                # D(x_i) vs oracle samples
+            aes.ecb(rk, g, True, out=pt, **kw)                            # D(x_i) vs oracle samples
         s.synchronize()
         checked += golden.check("ecb_dec", KEYBITS, first, n, gather(pt))
         return ok and checked >= 6
@@ -278,18 +334,23 @@ def _e2e(aes, pdist, key, rk, x, ct, pt, nbytes, K, dev):
     hc = torch.empty_like(hx).pin_memory()
     hp = torch.empty_like(hx).pin_memory()
     pipe = aes.Pipeline(chunk_bytes=64 << 20, depth=4)
-    pipe.run(rk, hx, hc)
-    pipe.run(rk, hc, hp, decrypt=True)
+    passes = 2 if DIR == "both" else 1
+
+    def one(r):
+        if DIR in ("both", "enc"):
+            pipe.run(r, hx, hc)
+        if DIR in ("both", "dec"):
+            pipe.run(r, hc if DIR == "both" else hx, hp, decrypt=True)
+    one(rk)
     KE = max(1, min(K, 5))
     pdist.barrier(dev)
     t0 = time.perf_counter()
     for _ in range(KE):
-        r = aes.expand_key(key)
-        pipe.run(r, hx, hc)
-        pipe.run(r, hc, hp, decrypt=True)
+        one(aes.expand_key(key))
     dt = pdist.max_over_ranks(time.perf_counter() - t0, dev)
     pipe.close()
-    assert torch.equal(hp, hx)
+    if DIR == "both":
+        assert torch.equal(hp, hx)
     s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     tl = []
     for _ in range(3):
@@ -302,12 +363,12 @@ def _e2e(aes, pdist, key, rk, x, ct, pt, nbytes, K, dev):
         torch.cuda.synchronize(dev)
         tl.append(time.perf_counter() - t0)
     link = nbytes / min(tl) / 1e9
-    return {"value": 8 * pdist.sum_over_ranks(2.0 * nbytes * KE, dev) / dt / 1e9, "unit": "Gbps",
-            "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": 2 * nbytes,
+    return {"value": 8 * pdist.sum_over_ranks(passes * nbytes * KE, dev) / dt / 1e9, "unit": "Gbps",
+            "h2d_bytes_per_step": passes * nbytes, "d2h_bytes_per_step": passes * nbytes,
             "steps": KE, "timing": "host perf_counter around synchronous aes_pipeline_run calls, max over ranks",
             "path": "aes_pipeline_run: pinned host -> H2D -> kernel -> D2H, 64 MiB chunks x 4 streams",
             "link_GBps_each_direction": link,
-            "link_frac": (2.0 * nbytes * KE / dt / 1e9) / link}   # bytes each way per second / ceiling
+            "link_frac": (passes * nbytes * KE / dt / 1e9) / link}   # bytes each way per second / ceiling
 
 
 HYBRID_MIN_BLOCKS = 1 << 23    # aes_ecb.cu kHybridMinBlocks: the default kernel from here up is the hybrid one
@@ -352,9 +413,10 @@ def _rooflines(n, enc_ms, dec_ms, lds_peak, nsm, clocks):
     peak, peak_src, _ = measured_peaks()
     kern_ms = max(enc_ms, dec_ms)
     dom = "encrypt" if enc_ms >= dec_ms else "decrypt"
-    hybrid = n >= HYBRID_MIN_BLOCKS
-    kname = (f"hybrid_kernel<10,{dom}> (aes_ecb_{dom}: 28 T-table + 4 bitsliced warps per CTA)" if hybrid
-             else f"ecb_kernel<10,{dom}> (aes_ecb_{dom})")
+    hybrid = VARIANT == "hybrid" or (VARIANT == "default" and SPT in (0, 1) and n >= HYBRID_MIN_BLOCKS)
+    kname = (f"hybrid_kernel<{NR},{dom}> (aes_ecb_{dom}: 28 T-table + 4 bitsliced warps per CTA)" if hybrid
+             else f"bs_kernel<{NR},{dom}> (bitsliced only)" if VARIANT == "bitslice"
+             else f"ecb_kernel<{NR},{dom}> (aes_ecb_{dom}, variant {VARIANT})")
     achieved = 32.0 * n / (kern_ms * 1e-3) / 1e9               # GB/s, 16 B read + 16 B written per block
     traffic, traffic_src = ncu_traffic(32 * n)
     lookups = 16 * NR * n
@@ -411,7 +473,7 @@ def run_ours(a):
     pt = torch.empty_like(x)
     s = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(s):
-        synth.fill_device(x, first_block=first)
+        synth.fill_device(x, first_block=first, **({} if SEED is None else {"seed": SEED}))
     s.synchronize()
 
     ok = _parity_gate(aes, golden, rk, x, ct, pt, s, first, n, dev, rank)
@@ -425,20 +487,24 @@ def run_ours(a):
 
     # ---- the step: A1/A2 on the host, then the two kernels -----------------
     nvtx = torch.cuda.nvtx
+    kw = _kernel_kw()
+    passes = 2 if DIR == "both" else 1
 
     def step(ev=None):
         nvtx.range_push("aes step")
         r = aes.expand_key(key)
         if ev:
             ev[0].record(s)
-        nvtx.range_push("aes_ecb_encrypt")
-        aes.ecb_encrypt(r, x, out=ct)
-        nvtx.range_pop()
+        if DIR in ("both", "enc"):
+            nvtx.range_push("aes_ecb_encrypt")
+            aes.ecb(r, x, False, out=ct, **kw)
+            nvtx.range_pop()
         if ev:
             ev[1].record(s)
-        nvtx.range_push("aes_ecb_decrypt")
-        aes.ecb_decrypt(r, ct, out=pt)
-        nvtx.range_pop()
+        if DIR in ("both", "dec"):
+            nvtx.range_push("aes_ecb_decrypt")
+            aes.ecb(r, ct if DIR == "both" else x, True, out=pt, **kw)
+            nvtx.range_pop()
         if ev:
             ev[2].record(s)
         nvtx.range_pop()
@@ -473,9 +539,10 @@ def run_ours(a):
     ms = pdist.max_over_ranks(ms_local, dev)
     enc_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
     dec_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
-    total_payload = pdist.sum_over_ranks(2.0 * nbytes * K, dev)
+    total_payload = pdist.sum_over_ranks(passes * nbytes * K, dev)
     gbps = 8 * total_payload / (ms * 1e-3) / 1e9
-    assert torch.equal(pt, x)             # decrypt(encrypt(x)) == x after the timed region too
+    if DIR == "both":
+        assert torch.equal(pt, x)         # decrypt(encrypt(x)) == x after the timed region too
 
     # context (not the metric): the NEXT-1 CTR kernel on the same buffer, event-timed
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -510,23 +577,28 @@ def run_ours(a):
                                "note": "one thread: the analogue of the paper's 'standard C' CPU column (PAPER.md:473)"}}
 
     if rank == 0:
+        line_seed = synth.DATA_SEED if SEED is None else SEED
         l2 = torch.cuda.get_device_properties(dev).L2_cache_size
         line = {
             "metric": METRIC, "value": gbps, "unit": "Gbps", "n_gpus": world, "steps": K, "warmup": a.warmup,
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u8", "data": "synthetic (splitmix64 counter stream, seed 190205234; random-init key)",
+            "dtype": "u8", "data": f"synthetic (splitmix64 counter stream, seed {line_seed}; random-init key)",
             "config": {"workload": WORKLOAD if nbytes == GIB else WORKLOAD.replace("1 GiB", f"{nbytes / GIB:g} GiB"),
                        "keybits": KEYBITS, "bytes_per_gpu": nbytes,
                        "global_bytes": nbytes * world, "parallelism": f"dp{world} (contiguous block shards)",
-                       "step": f"expand_key + encrypt({nbytes / GIB:g} GiB) + decrypt({nbytes / GIB:g} GiB)",
+                       "step": " + ".join(["expand_key"] + [f"{d}({nbytes / GIB:g} GiB)" for d, on in
+                                                            (("encrypt", DIR != "dec"), ("decrypt", DIR != "enc")) if on]),
                        "l2": (f"inputs ({nbytes / 2**20:.0f} MiB) larger than L2 ({l2 / 2**20:.0f} MiB); no flush"
                               if nbytes > l2 else "inputs smaller than L2 (harness-test size): L2-warm"),
-                       "variant": ("default = hybrid: 28 T-table warps (lane-replicated smem tables) + 4 bitsliced "
+                       "variant": (f"{VARIANT} (spt {SPT or 1})" if _kernel_kw() else
+                                   "default = hybrid: 28 T-table warps (lane-replicated smem tables) + 4 bitsliced "
                                    "warps per 1024-thread CTA, persistent grid" if n >= HYBRID_MIN_BLOCKS else
-                                   "default = smem_repl, 1 state/thread, persistent grid")},
+                                   "default = smem_repl, 1 state/thread, persistent grid"),
+                       "seed": synth.DATA_SEED if SEED is None else SEED},
             "GBps": gbps / 8, "enc_ms": enc_ms, "dec_ms": dec_ms,
-            "enc_Gbps": 8 * nbytes / (enc_ms * 1e-3) / 1e9, "dec_Gbps": 8 * nbytes / (dec_ms * 1e-3) / 1e9,
-            "hbm_frac_step": (32.0 * n * 2 * K / (ms_local * 1e-3) / 1e9) / peak,
+            "enc_Gbps": 8 * nbytes / (enc_ms * 1e-3) / 1e9 if DIR != "dec" else None,
+            "dec_Gbps": 8 * nbytes / (dec_ms * 1e-3) / 1e9 if DIR != "enc" else None,
+            "hbm_frac_step": (32.0 * n * passes * K / (ms_local * 1e-3) / 1e9) / peak,
             "roofline": roof, "roofline_lds": roof_lds, "roofline_hybrid": roof_hyb,
             "roofline_note": ("T-table AES does 16*Nr shared-memory lookups per 32 HBM bytes, so the binding "
                               "roofline is the shared-memory gather rate (roofline_lds), not HBM (T-table AES-128 "
@@ -534,7 +606,7 @@ def run_ours(a):
                               "lookup-free bitsliced warps on the idle ALU, bounded jointly by the data path and "
                               "the ALU pipe (roofline_hybrid; DESIGN.md 6, 11)"),
             "cpu_baseline": cpu, "e2e": e2e,
-            "clocks": clocks, "gpu_launches": 2 * K, "gpu": torch.cuda.get_device_name(dev),
+            "clocks": clocks, "gpu_launches": passes * K, "gpu": torch.cuda.get_device_name(dev),
             "wall_window_ms_rank0": wall_ms, "ranks": ranks,
             "context": {"ctr_aes128_Gbps": ctr_gbps,
                         "note": "NEXT-1 CTR (counter-mode caching) on the same 1 GiB buffer; not part of `value`"},

@@ -70,6 +70,9 @@ def init(backend: str | None = None):
         if backend is None:
             backend = "nccl" if torch.cuda.is_available() else "gloo"
         if backend == "nccl":
+            if world > torch.cuda.device_count():
+                raise SystemExit(f"[dist] {world} ranks but {torch.cuda.device_count()} visible GPU(s): NCCL needs "
+                                 "one GPU per rank (for a harness run on fewer GPUs set AES_BENCH_BACKEND=gloo)")
             local = local % max(1, torch.cuda.device_count())
             torch.cuda.set_device(local)
             dist.init_process_group(backend, device_id=torch.device("cuda", local))

@@ -85,3 +85,40 @@ def test_bench_gpus_2_without_torchrun_spawns_its_ranks():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["ranks"]["world"] == 2 and d["ranks"]["backend"] == "gloo"
     assert d["ranks"]["kernel_ms_min"] <= d["ranks"]["kernel_ms_max"]
+
+
+def test_reference_arm_flags_relabel_on_cpu():
+    """--keybits / --dir / --seed reach the reference arm: metric and workload
+    are relabelled, the oracle runs that direction on that stream."""
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0",
+                        "--ref-seconds", "1", "--keybits", "256", "--dir", "dec", "--seed", "7"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = _last_json(r.stdout)
+    assert d["metric"].startswith("AES-256 ECB decrypt Gbps") and d["config"]["keybits"] == 256
+    assert "AES-256 ECB decrypt," in d["config"]["workload"] and "seed 7" in d["data"]
+    assert "decrypt" in d["cpu_baseline"]["sample"] and "+" not in d["cpu_baseline"]["sample"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("flags,keybits,passes", [
+    (["--keybits", "256", "--dir", "dec", "--variant", "smem_repl"], 256, 1),
+    (["--keybits", "192", "--dir", "enc", "--variant", "hybrid", "--seed", "12345"], 192, 1),
+    (["--variant", "smem_repl", "--spt", "2"], 128, 2),
+])
+def test_bench_flags(flags, keybits, passes):
+    """SURVEY.md 5 "Config / flags": --keybits/--dir/--variant/--spt/--seed on
+    our arm, parity-gated (the golden samples on the sampled stream in the same
+    kernel configuration, the round trip on the --seed stream)."""
+    nbytes = 32 << 20
+    r = subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--bytes-per-gpu", str(nbytes),
+                        "--no-cpu", *flags], cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _last_json(r.stdout)
+    assert "error" not in d and d["value"] > 100
+    assert d["config"]["keybits"] == keybits and d["metric"].startswith(f"AES-{keybits} ECB")
+    assert d["e2e"]["h2d_bytes_per_step"] == passes * nbytes
+    if "--variant" in flags:
+        assert d["config"]["variant"].startswith(flags[flags.index("--variant") + 1])
+    if "--seed" in flags:
+        assert d["config"]["seed"] == 12345

@@ -40,7 +40,13 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", 1)))
+    ap.add_argument("--keybits", type=int, default=128, choices=[128, 192, 256])
+    ap.add_argument("--dir", default="enc", choices=["enc", "dec"], help="the timed in-place operation")
+    ap.add_argument("--variant", default="default", choices=["default", "smem_repl", "hybrid", "bitslice"])
     a = ap.parse_args()
+    kw = {} if a.variant == "default" else {"variant": {"smem_repl": aes.AES_VAR_SMEM_REPL,
+                                                        "hybrid": aes.AES_VAR_HYBRID,
+                                                        "bitslice": aes.AES_VAR_BITSLICE}[a.variant]}
     rc = pdist.respawn_under_torchrun(a.gpus, [os.path.abspath(__file__), *sys.argv[1:]])
     if rc is not None:
         return rc
@@ -51,27 +57,27 @@ def main():
     n = a.global_bytes // 16
     b0, b1 = pdist.shard_range(n, rank, world)
     m = b1 - b0
-    key = synth.key(128)
+    key = synth.key(a.keybits)
     rk = aes.expand_key(key)
     x = torch.empty(16 * m, dtype=torch.uint8, device=dev)
     s = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(s):
         synth.fill_device(x, first_block=b0)
-        aes.ecb_encrypt(rk, x, out=x)
+        aes.ecb(rk, x, False, out=x, **kw)
     s.synchronize()
     # sampled parity: oracle-written golden samples (incl. shard edges and block
     # 2^32-1) for E(x); after an in-place decrypt the same samples must be the input
     gather = lambda loc: x.view(-1, 16)[torch.from_numpy(loc).to(dev)].cpu().numpy()
     try:
-        checked = golden.check("ecb_enc", 128, b0, m, gather)
+        checked = golden.check("ecb_enc", a.keybits, b0, m, gather)
         ok = checked >= 3
     except AssertionError as e:
         print(f"[rank {rank}] {e}", file=sys.stderr)
         ok = False
-    idx, _ = golden.samples("ecb_enc", 128)
+    idx, _ = golden.samples("ecb_enc", a.keybits)
     g = idx[(idx >= np.uint64(b0)) & (idx < np.uint64(b1))]
     with torch.cuda.stream(s):
-        aes.ecb_decrypt(rk, x, out=x)
+        aes.ecb(rk, x, True, out=x, **kw)
     s.synchronize()
     ok &= bool(np.array_equal(gather((g - np.uint64(b0)).astype(np.int64)), synth.blocks_at(g)))
     if pdist.sum_over_ranks(0.0 if ok else 1.0, dev):
@@ -80,7 +86,7 @@ def main():
         return 1
     with torch.cuda.stream(s):
         for _ in range(a.warmup):
-            aes.ecb_encrypt(rk, x, out=x)
+            aes.ecb(rk, x, a.dir == "dec", out=x, **kw)
     s.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     pdist.barrier(dev)
@@ -88,7 +94,7 @@ def main():
     with torch.cuda.stream(s):
         e0.record(s)
         for _ in range(a.steps):
-            aes.ecb_encrypt(rk, x, out=x)
+            aes.ecb(rk, x, a.dir == "dec", out=x, **kw)
         e1.record(s)
     s.synchronize()
     pdist.barrier(dev)
@@ -99,7 +105,11 @@ def main():
     total = pdist.sum_over_ranks(16.0 * m * a.steps, dev)
     if rank == 0:
         gbps = 8 * total / (ms * 1e-3) / 1e9
-        print(json.dumps({"metric": "AES-128 ECB encrypt Gbps, 64 GiB sharded (BASELINE config 5)",
+        what = "encrypt" if a.dir == "enc" else "decrypt"
+        print(json.dumps({"metric": f"AES-{a.keybits} ECB {what} Gbps, {a.global_bytes / 2**30:g} GiB sharded"
+                                    + (" (BASELINE config 5)" if (a.keybits, a.dir, a.global_bytes) == (128, "enc", 64 << 30)
+                                       else ""),
+                          "variant": a.variant,
                           "value": gbps, "unit": "Gbps", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
                           "ms_per_step": ms / a.steps, "scaling": "strong", "global_bytes": a.global_bytes,
                           "bytes_per_gpu": 16 * m, "GBps": gbps / 8,
