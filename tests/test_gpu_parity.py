@@ -575,6 +575,76 @@ def test_cuda_graph_capture_and_replay(aes):
         assert np.array_equal(ks.cpu().numpy(), oracle.ctr(key, iv, host, nthreads=8))
 
 
+def test_hybrid_threads_streams_and_graph(aes):
+    """The hybrid kernel (bitsliced round keys built per call on the host,
+    per-CTA unit queue) from 6 host threads on their own streams with
+    different keys, and captured into a CUDA graph (CTR / CBC through the
+    crossover knob at capture time) and replayed on fresh inputs."""
+    import os
+    import threading
+    n = 16 * 1024 + 77                      # one CTA: both warp kinds take units
+    host = synth.blocks(0, n)
+    x = _dev_rand(n)
+    results, errors = {}, []
+
+    def work(t):
+        try:
+            kb = (128, 192, 256)[t % 3]
+            key = bytes((t * 17 + i) & 0xFF for i in range(kb // 8))
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(10):
+                    rk = aes.expand_key(key)
+                    ct = aes.ecb_encrypt(rk, x, variant=aes.AES_VAR_HYBRID, grid=1)
+                    back = aes.ecb_decrypt(rk, ct, variant=aes.AES_VAR_HYBRID, grid=1)
+            s.synchronize()
+            results[t] = (key, ct.cpu().numpy(), bool(torch.equal(back, x)))
+        except Exception as e:   # pragma: no cover
+            errors.append(e)
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(6)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors
+    for t, (key, ct, ok) in results.items():
+        assert ok
+        assert np.array_equal(ct, oracle.encrypt(key, host, nthreads=4)), t
+
+    key = synth.key(192)
+    rk = aes.expand_key(key)
+    iv = bytes(range(16))
+    m = 3 * 2**20 + 5                       # default grid, > kTailUnits units per CTA
+    y = _dev_rand(m)
+    ct, pt, ks, cb = (torch.empty_like(y) for _ in range(4))
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    os.environ["AES_B200_HYBRID_MIN_BLOCKS"] = "0"
+    try:
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                aes.ecb_encrypt(rk, y, out=ct)
+                aes.ecb_decrypt(rk, ct, out=pt)
+                aes.ctr_xcrypt(rk, iv, y, out=ks)
+                aes.cbc_decrypt(rk, iv, y, out=cb)
+    finally:
+        os.environ.pop("AES_B200_HYBRID_MIN_BLOCKS", None)
+    for first in (5, 999):
+        synth.fill_device(y, first_block=first)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        hy = synth.blocks(first, m)
+        sel = np.r_[0:4096, m - 4096:m]
+        assert np.array_equal(ct.cpu().numpy().reshape(-1, 16)[sel],
+                              oracle.encrypt(key, hy.reshape(-1, 16)[sel].copy().reshape(-1), nthreads=8).reshape(-1, 16))
+        assert torch.equal(pt, y)
+        assert np.array_equal(ks.cpu().numpy(), oracle.ctr(key, iv, hy, nthreads=16))
+        assert np.array_equal(cb.cpu().numpy(), _cbc_decrypt_oracle(key, iv, hy))
+
+
 def test_cli_file_round_trip(aes, tmp_path):
     """python -m paper_1902_05234_b200 enc/dec on a non-block-multiple file
     (PKCS#7): ciphertext equals OpenSSL-free oracle ECB of the padded file,
