@@ -122,3 +122,22 @@ def test_bench_flags(flags, keybits, passes):
         assert d["config"]["variant"].startswith(flags[flags.index("--variant") + 1])
     if "--seed" in flags:
         assert d["config"]["seed"] == 12345
+
+
+def test_hybrid_ceiling_solves_both_resource_equations():
+    """roofline_hybrid: the T-table / bitsliced block mix saturates the L1 data
+    path (32 lane-slots/clk/SM) and the ALU pipe (64 lane-ops/clk/SM) at once,
+    with the per-block counts of profiles/r02_sass_counts.json; the joint
+    ceiling lies above the T-table-only one (32 / (L_T + 8) blocks/clk/SM)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    for dom, key in (("encrypt", "nr10_enc"), ("decrypt", "nr10_dec")):
+        h = bench._hybrid_ceiling(dom, {"sm_mhz": 1965.0}, 148)
+        c = json.load(open(os.path.join(ROOT, "profiles", "r02_sass_counts.json")))[key]
+        LT, AT = c["t_table_per_block"]["lds"], c["t_table_per_block"]["alu"]
+        AB = c["bitsliced_per_block"]["alu"]
+        tot = h["peak_blocks_per_clk_per_sm"]
+        t, b = tot * h["t_share"], tot * (1 - h["t_share"])
+        assert abs((LT + 8) * t + 8 * b - 32) < 1e-9 and abs(AT * t + AB * b - 64) < 1e-9
+        assert 0 < b < t and tot > 32 / (LT + 8)
+        assert abs(h["peak_GBps_payload"] - 16 * tot * 148 * 1.965e9 / 1e9) < 1e-6
