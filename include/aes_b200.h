@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define AES_B200_ABI_VERSION 2   /* 2: AES_VAR_GLOBAL, aes_launch_config.flags, AES_ECAPTURE */
+#define AES_B200_ABI_VERSION 3   /* 2: AES_VAR_GLOBAL, aes_launch_config.flags, AES_ECAPTURE; 3: AES_VAR_HYBRID, AES_VAR_BITSLICE (hybrid default from 2^23 blocks) */
 
 typedef enum {
     AES_OK = 0,

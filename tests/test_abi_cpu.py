@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     lib = ctypes.CDLL(_native.LIB_PATH)
     for name in declared:
         assert hasattr(lib, name), name
-    assert _native.lib.aes_abi_version() == 2
+    assert _native.lib.aes_abi_version() == 3
 
 
 def test_library_is_sm100a_and_has_no_oracle_symbols():
