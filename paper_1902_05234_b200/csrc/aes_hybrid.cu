@@ -42,6 +42,10 @@
 #include "aes_device.cuh"
 #include "aes_host.h"
 
+#ifndef AES_HYB_STEP
+#define AES_HYB_STEP 2
+#endif
+
 namespace aesb200 {
 
 constexpr int kHybT = 28;                  // T-table warps per CTA (7 warpgroups)
@@ -52,6 +56,7 @@ static_assert(kHybT % 4 == 0 && kHybB % 4 == 0, "setmaxnreg acts on whole warpgr
 constexpr uint64_t kUnit = 32;             // blocks per unit
 constexpr uint64_t kSuper = 64;            // units per super-chunk (2048 blocks = 32 KiB)
 constexpr uint64_t kTailUnits = 384;       // bitsliced warps stop claiming this close to the end
+constexpr int kStep = AES_HYB_STEP;        // units per T-table claim (ECB / CBC); 4 measured 1 % slower
 // The unit counter is 32-bit (a native shared-memory ATOMS.ADD; the 64-bit
 // one is a CAS loop): launch() falls back to the T-table kernel when a CTA
 // would need 2^31 units or more (2^36 blocks = 1 TiB per CTA).
@@ -140,42 +145,50 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (MODE == M_CBCD) y = xor4(y, i ? __ldg(in + i - 1) : make_uint4(mp.iv[0], mp.iv[1], mp.iv[2], mp.iv[3]));
             return y;
         };
-        // Two units (blocks b .. b+63: kSuper is even) per claim, claimed one
+        // kStep units (blocks b .. b + 32*kStep - 1: every claim is a multiple of
+        // kStep and kSuper is too, so they are contiguous) per claim, claimed one
         // step ahead: the atomic for step t+2 is issued before step t's rounds
         // and its result is read (shfl) only after them, so its latency hides.
+        constexpr uint64_t W = kStep * kUnit;
         uint32_t a = 0;
-        if (lane == 0) a = atomicAdd(&q_next, 2u);
+        if (lane == 0) a = atomicAdd(&q_next, (uint32_t)kStep);
         const uint32_t ucur = __shfl_sync(0xffffffffu, a, 0);
-        if (lane == 0) a = atomicAdd(&q_next, 2u);
+        if (lane == 0) a = atomicAdd(&q_next, (uint32_t)kStep);
         uint32_t unxt = __shfl_sync(0xffffffffu, a, 0);
         uint64_t b = unit_block(ucur);
         if (b >= n) return;
-        if (b + 2 * kUnit <= n) {
+        if (b + W <= n) {
             // whole steps: no per-lane bounds checks (the unit sequence is
             // increasing, so once a step is not whole every later one is past n)
-            uint4 v0 = t_in(b + lane), v1 = t_in(b + kUnit + lane);
+            uint4 v[kStep];
+#pragma unroll
+            for (int k = 0; k < kStep; k++) v[k] = t_in(b + k * kUnit + lane);
             for (;;) {                      // the next step's states load during this step's rounds
                 const uint64_t nb = unit_block(unxt);
-                if (nb + 2 * kUnit > n) {
-                    __stcs(out + b + lane, t_out(b + lane, v0));
-                    __stcs(out + b + kUnit + lane, t_out(b + kUnit + lane, v1));
+                if (nb + W > n) {
+#pragma unroll
+                    for (int k = 0; k < kStep; k++) __stcs(out + b + k * kUnit + lane, t_out(b + k * kUnit + lane, v[k]));
                     b = nb;
                     break;
                 }
-                const uint4 n0 = t_in(nb + lane), n1 = t_in(nb + kUnit + lane);
-                if (lane == 0) a = atomicAdd(&q_next, 2u);
-                __stcs(out + b + lane, t_out(b + lane, v0));
-                __stcs(out + b + kUnit + lane, t_out(b + kUnit + lane, v1));
+                uint4 nv[kStep];
+#pragma unroll
+                for (int k = 0; k < kStep; k++) nv[k] = t_in(nb + k * kUnit + lane);
+                if (lane == 0) a = atomicAdd(&q_next, (uint32_t)kStep);
+#pragma unroll
+                for (int k = 0; k < kStep; k++) __stcs(out + b + k * kUnit + lane, t_out(b + k * kUnit + lane, v[k]));
                 unxt = __shfl_sync(0xffffffffu, a, 0);
                 b = nb;
-                v0 = n0;
-                v1 = n1;
+#pragma unroll
+                for (int k = 0; k < kStep; k++) v[k] = nv[k];
             }
         }
         if (b < n) {                        // the one partial step (ragged end of the message)
-            const uint64_t i = b + lane;
-            if (i < n) __stcs(out + i, t_out(i, t_in(i)));
-            if (i + kUnit < n) __stcs(out + i + kUnit, t_out(i + kUnit, t_in(i + kUnit)));
+#pragma unroll
+            for (int k = 0; k < kStep; k++) {
+                const uint64_t i = b + k * kUnit + lane;
+                if (i < n) __stcs(out + i, t_out(i, t_in(i)));
+            }
         }
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegB));
