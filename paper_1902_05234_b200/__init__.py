@@ -127,7 +127,9 @@ def _check_tensor(x, name):
 def ecb(rk: RoundKeys, x, decrypt: bool, out=None, variant: int = AES_VAR_DEFAULT,
         states_per_thread: int = 0, grid: int = 0, stream=None, flags: int = 0):
     """ECB over a device buffer; ``out`` may be ``x`` (in place) or None (new tensor).
-    ``flags``: AES_LAUNCH_* bits (aes_launch_config.flags)."""
+    ``variant``: AES_VAR_* (default: the hybrid T-table + bitsliced kernel from
+    2^23 blocks, the replicated T-table kernel below); ``flags``: AES_LAUNCH_*
+    bits (aes_launch_config.flags).  Every variant returns identical bytes."""
     import torch
     _check_tensor(x, "x")
     if out is None:
