@@ -10,7 +10,6 @@ its parity with the oracle on arbitrary global offsets (test_gpu_parity).
 import os
 import socket
 
-import numpy as np
 import pytest
 import torch
 import torch.distributed as dist

@@ -56,7 +56,6 @@ for v, name in ((aes.AES_VAR_SMEM_REPL, "t_table"), (aes.AES_VAR_HYBRID, "hybrid
         code = _native.lib.aes_ecb_launch(rk.c_ref, rk.nr, 0, hx.data_ptr(), ho.data_ptr(), G // 16, sp,
                                           ctypes.byref(cfg))
         assert code == 0, code
-    import ctypes  # noqa: E402
     ho.zero_()
     zc()
     torch.cuda.synchronize()
