@@ -176,8 +176,9 @@ aes_status aes_ecb_batch(const aes_round_keys *keys, int nkeys, int decrypt, con
  *                       leave idle; both take 32-block units from a per-CTA
  *                       queue.  states_per_thread must be 1.
  *  AES_VAR_BITSLICE   : every warp bitsliced (8 blocks per thread), no tables;
- *                       the ALU-only point of the ablation.  states_per_thread
- *                       must be 1. */
+ *                       the ALU-only point of the ablation (about half the
+ *                       T-table rate; no data-dependent memory access or
+ *                       branch).  states_per_thread must be 1. */
 typedef enum {
     AES_VAR_DEFAULT = 0,
     AES_VAR_SMEM_REPL = 1,
